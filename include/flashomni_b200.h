@@ -1,0 +1,140 @@
+/*
+ * flashomni_b200.h — C ABI of the B200-native FlashOmni hot path.
+ *
+ * Everything is plain pointers, sizes and a cudaStream_t passed as void*;
+ * all buffers are caller-allocated device memory and every call is
+ * stream-ordered (nothing synchronises, nothing allocates). Device-detected
+ * contract violations (an active query block with every key block skipped,
+ * a cold cache entry, a non-uniform pool group, stale symbols) set bits in
+ * a caller-owned uint32 status word in device memory; the host wrapper reads
+ * it and raises the matching exception of reference errors.py:4-25.
+ *
+ * Layouts (bf16 unless stated):
+ *   q, k, v, o        [seq, heads, 128]         token-major, = [seq, heads*128]
+ *   x                 [seq, d_model]
+ *   w_qt              [heads*128, d_model]      (reference w_q [heads, d_model, 128], transposed)
+ *   w_outt            [d_model, heads*128]      (reference w_out [heads, 128, d_model], transposed)
+ *   cache (diff stacks) [order_d+1, seq, heads*128]
+ *   bias  (B_c)       [order_d+1, seq, d_model]
+ *   valid             int32 [heads, rows]       valid difference orders per (head, block)
+ *   s_c               uint8 [heads, ceil(ceil(rows/pool_n)/8)]
+ *   s_s               uint8 [heads, ceil(rows/pool_n), ceil(ceil(cols/pool_n)/8)]
+ * Blocks are b_q = b_k = 128 tokens; rows = cols = ceil(seq/128).
+ */
+#ifndef FLASHOMNI_B200_H
+#define FLASHOMNI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FO_API __attribute__((visibility("default")))
+#else
+#define FO_API
+#endif
+
+/* return codes, one per reference exception class (errors.py:4-25) */
+enum {
+  FO_OK = 0,
+  FO_ERR_SHAPE = 1,       /* ShapeError */
+  FO_ERR_PARAM = 2,       /* ParameterError */
+  FO_ERR_BOUNDS = 3,      /* BoundsError */
+  FO_ERR_CONSISTENCY = 4, /* ConsistencyError */
+  FO_ERR_STATE = 5,       /* StateError */
+  FO_ERR_CUDA = 6         /* launch / driver failure */
+};
+/* device status-word bits */
+#define FO_ST_CONSISTENCY 0x1u
+#define FO_ST_STATE 0x2u
+#define FO_ST_BOUNDS 0x4u
+#define FO_ST_PARAM 0x8u
+#define FO_ST_TIMEOUT 0x10u
+
+FO_API int fo_abi_version(void);
+FO_API const char* fo_last_error(void);
+FO_API int fo_num_sms(void);
+
+/* Schedule workspace for one layer's symbols (plan): byte size and the byte
+ * offsets of {counts, items, gemm-q items, head masks, orders, pairs}. */
+FO_API size_t fo_plan_workspace_bytes(int heads, int rows);
+FO_API void fo_plan_offsets(int heads, int rows, size_t offsets[6]);
+
+/* K1 symbol pack. Replaces encode_cache_mask / encode_skip_mask / build_symbols
+ * (reference pkg/src/omniattn/symbols.py:65-81,145-160) for all heads at once.
+ * cache_bits uint8 [heads, rows], skip_bits uint8 [heads, rows, cols] (nonzero = 1). */
+FO_API int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int heads, int rows,
+                      int cols, int pool_n, uint8_t* s_c, uint8_t* s_s, uint32_t* status,
+                      void* stream);
+
+/* Device decode of every cache bit and pair bit with the same decoders the kernel
+ * prologues use. Replaces decode_spatial / decode_reduction / decode_run
+ * (symbols.py:163-198). active uint8 [heads, rows], pair_bits uint8 [heads, rows, cols]. */
+FO_API int fo_decode_symbols(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols,
+                      int pool_n, uint8_t* active, uint8_t* pair_bits, void* stream);
+
+/* Build the layer schedule from symbols: attention work items sorted by KV
+ * count, GEMM-Q tile list, per-block head masks, cached-bias orders and the
+ * mask-predicted pair counts. Raises CONSISTENCY for an active row with no key
+ * block (pyref.py:43-46) and STATE for a cached tile with a cold cache
+ * (attention.py:208-211, gemm.py:150-153) when `valid` is given.
+ * dense=1 schedules every (head, block) with every key block (update step). */
+FO_API int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols, int pool_n,
+            int dense, const int32_t* valid, int order_d, void* plan_ws, uint32_t* status,
+            void* stream);
+
+/* K2 / K2u sparse attention for all heads. Replaces sparse_attention(mode="bias")
+ * (attention.py:150-221) and the backend entry masked_block_attention
+ * (_kernels/pyref.py:14-48, _kernels/_core.pyx:14-101). Rows of cached blocks
+ * are left untouched in `out`. update_mode=1 (plan built dense) also pushes
+ * every tile into the diff stacks `cache` and bumps `valid`
+ * (attention.py:71-85 via pipeline.py:274-278). pairs (int64 [heads], may be
+ * NULL) accumulates the instrumented computed-pair count. */
+FO_API int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, int heads,
+                        int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                        const void* plan_ws, float scale, int update_mode, void* out, void* cache,
+                        int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
+                        void* stream);
+
+/* OP_reuse for mode="materialize": cached tiles of `out` <- sum_d coef[d]*stack[d]
+ * (attention.py:96-113,212-216). coef is a host array of order_d+1 floats. */
+FO_API int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim, int rows,
+                            int order_d, const void* plan_ws, const int32_t* valid,
+                            const float* coef, void* out, void* stream);
+
+/* FeatureCache.update for the selected (head, block) entries (select uint8
+ * [heads, rows], NULL = all) (attention.py:71-85,128-131). */
+FO_API int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,
+                  int rows, int order_d, const uint8_t* select, void* stream);
+
+/* K3 GEMM-Q: q = rope(rms_norm(x @ W_q[h])) for active (block, head) tiles only
+ * (gemm.py:44-93, tensor.py:68-109). dense=1: every tile (update phase, plan
+ * may be NULL). rope_cos/rope_sin fp32 [seq, 64] = cos/sin(pos * 1e4^(-2j/128)). */
+FO_API int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, int head_dim,
+              const float* norm_w, const float* rope_cos, const float* rope_sin, float eps,
+              const void* plan_ws, int dense, void* q_out, void* stream);
+
+/* K5 GEMM-O update: out = sum_h o_h W_h, B_c[d] = sum_{h cached next} stack_d^h W_h
+ * (gemm.py:110-175). plan_ws is the plan of the NEXT symbols built with `valid`;
+ * orders are taken from it. */
+FO_API int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int seq, int heads,
+                     int head_dim, int d_model, int order_d, const void* plan_ws, void* out,
+                     void* bias, uint32_t* status, void* stream);
+
+/* K4 GEMM-O dispatch: out = sum_{h active} o_h W_h + sum_d coef[d] * B_c[d]
+ * (gemm.py:178-229). orders int32 [rows] from the update step; coef host floats. */
+FO_API int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, const int32_t* orders,
+                       int seq, int heads, int head_dim, int d_model, int order_d,
+                       const float* coef, const void* plan_ws, void* out, void* stream);
+
+/* Stale-symbol check (gemm.py:201-209): STATE if the decoded cache bits differ. */
+FO_API int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
+                          int pool_n, uint32_t* status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHOMNI_B200_H */

@@ -1,0 +1,69 @@
+"""FlashOmni hot path, B200-native (sm_100a tcgen05/TMEM/TMA kernels).
+
+Drop-in for the operator API of the reference `omniattn` package
+(pkg/src/omniattn/__init__.py): sparse-symbol codec, sparse_attention,
+GEMM-Q (project_q), GEMM-O (project_out_update / project_out_dispatch) and the
+feature cache — batched over heads and resident in HBM. The compute runs in
+the C-ABI library `_fo_b200.so` (include/flashomni_b200.h); there is no CPU
+fallback.
+"""
+
+from .errors import (
+    BoundsError,
+    ConsistencyError,
+    DeviceError,
+    EngineError,
+    ParameterError,
+    ShapeError,
+    StateError,
+)
+from .symbols import (
+    SYMBOL_FORMAT_VERSION,
+    DeviceSymbols,
+    SymbolBuffer,
+    build_symbols,
+    ceil_div,
+    decode_reduction,
+    decode_run,
+    decode_spatial,
+    encode_cache_mask,
+    encode_skip_mask,
+    encode_symbols,
+)
+from .attention import (
+    AttnCounters,
+    CacheEntry,
+    FeatureCache,
+    dense_attention_update,
+    forecast_coefficients,
+    sparse_attention,
+)
+from .gemm import (
+    CachedBias,
+    GemmCounters,
+    pack_w_out,
+    pack_w_q,
+    project_out_dispatch,
+    project_out_update,
+    project_q,
+    rope_tables,
+)
+from .pipeline import (
+    LayerParams,
+    LayerState,
+    dispatch_step,
+    new_layer_state,
+    project_kv,
+    shard_heads,
+    update_step,
+)
+from ._kernels import available_backends, get_backend
+
+__version__ = "0.1.0"
+
+
+def backend_name():
+    return "b200"
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]

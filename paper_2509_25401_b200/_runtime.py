@@ -1,0 +1,75 @@
+"""Device plumbing shared by the operators: tensor checks, the device status
+word that carries kernel-detected contract violations, and stream handles."""
+
+import torch
+
+from . import _lib
+from .errors import DeviceError, ParameterError, ShapeError
+
+TILE = 128  # b_q = b_k = head_dim the sm_100a kernels are built for
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 engine has no CPU fallback")
+    _lib.load()
+
+
+def as_device(t, dtype, name):
+    """Accept numpy arrays / CPU tensors by copying them to the current device
+    once; device tensors of the right dtype pass through untouched."""
+    require_cuda()
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    if t.device.type != "cuda":
+        t = t.to("cuda")
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+def check_bsd(t, name, seq=None, heads=None):
+    """[S, H, 128] token-major activations (a [S, H*128] view is accepted)."""
+    if t.dim() == 2:
+        if t.shape[1] % TILE:
+            raise ShapeError(f"{name}: width {t.shape[1]} not a multiple of {TILE}")
+        t = t.view(t.shape[0], t.shape[1] // TILE, TILE)
+    if t.dim() != 3:
+        raise ShapeError(f"{name}: expected [seq, heads, {TILE}], got {tuple(t.shape)}")
+    if t.shape[2] != TILE:
+        raise ParameterError(f"{name}: head_dim must be {TILE} for the sm_100a kernels, got {t.shape[2]}")
+    if seq is not None and t.shape[0] != seq:
+        raise ShapeError(f"{name}: seq {t.shape[0]} != {seq}")
+    if heads is not None and t.shape[1] != heads:
+        raise ShapeError(f"{name}: heads {t.shape[1]} != {heads}")
+    return t
+
+
+class Status:
+    """A uint32 status word in device memory; kernels OR error bits into it."""
+
+    _default = {}
+
+    def __init__(self, device=None):
+        self.t = torch.zeros(1, dtype=torch.int32, device=device or "cuda")
+
+    @classmethod
+    def default(cls):
+        dev = torch.cuda.current_device()
+        if dev not in cls._default:
+            cls._default[dev] = cls(device=f"cuda:{dev}")
+        return cls._default[dev]
+
+    def ptr(self):
+        return self.t.data_ptr()
+
+    def check(self, what):
+        """Synchronise on the word and raise the reference exception it encodes."""
+        bits = int(self.t.item())
+        if bits:
+            self.t.zero_()
+            _lib.raise_status(bits, what)
+
+
+def stream_ptr(stream=None):
+    return _lib.stream_handle(stream)

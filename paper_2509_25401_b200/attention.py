@@ -1,0 +1,308 @@
+"""Symbol-guided sparse attention and the feature cache, on the GPU.
+
+Mirrors reference pkg/src/omniattn/attention.py: each query block either runs
+compute-on-demand (online softmax over the key blocks its skip row allows) or
+cache-then-reuse (its tile is forecast from stored finite differences, or left
+alone in mode="bias" where the output projection covers it). The batched form
+processes every head of a layer in one launch: q, k, v are bf16 [seq, heads,
+128] CUDA tensors and `symbols` is a DeviceSymbols. The per-head reference
+signature (numpy q[n, d] + SymbolBuffer) is accepted too and adapted onto the
+batched kernel.
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._runtime import TILE, Status, check_bsd, require_cuda, stream_ptr
+from .errors import ParameterError, ShapeError, StateError
+from .symbols import DeviceSymbols, SymbolBuffer, ceil_div
+
+DTYPE = np.float32
+
+
+def forecast_coefficients(elapsed_k, interval_n, n_orders):
+    """(k/N)^d / d! in float32 (attention.py:88-93)."""
+    x = elapsed_k / interval_n
+    return np.array([x**d / math.factorial(d) for d in range(n_orders)], dtype=DTYPE)
+
+
+def check_elapsed(elapsed_k, interval_n):
+    if interval_n < 1 or not 1 <= elapsed_k <= interval_n - 1:
+        raise ParameterError(f"elapsed_k={elapsed_k} outside [1, {interval_n - 1}]")
+
+
+@dataclass
+class AttnCounters:
+    """Instrumentation for one attention call (attention.py:138-147)."""
+
+    pairs_total: int = 0
+    pairs_computed: int = 0
+
+    @property
+    def pairs_skipped(self):
+        return self.pairs_total - self.pairs_computed
+
+
+@dataclass
+class CacheEntry:
+    """Host view of one (head, block) entry (attention.py:58-69)."""
+
+    diff_stack: np.ndarray
+    valid_orders: int = 0
+
+
+class FeatureCache:
+    """Per (head, query block) backward-difference stacks for one layer, in HBM.
+
+    stacks: bf16 [order+1, seq, heads*128] — slot d holds the d-th backward
+    difference of every tile, laid out like the attention output so the GEMM-O
+    update reads it with the same TMA descriptor shape. valid: int32 [heads,
+    n_blocks] valid orders per entry (attention.py:116-135). Storage is
+    allocated on the first push (the sequence length comes from the tiles).
+    """
+
+    def __init__(self, heads, n_blocks, order, seq=None, device=None):
+        if order < 0 or order > 3:
+            raise ParameterError(f"order must be in [0, 3] on the B200 engine, got {order}")
+        require_cuda()
+        self.heads, self.n_blocks, self.order = int(heads), int(n_blocks), int(order)
+        self.device = device or "cuda"
+        self.valid = torch.zeros(self.heads, self.n_blocks, dtype=torch.int32, device=self.device)
+        self.stacks = None
+        self.seq = None
+        self.version = 0  # bumped on every push; keys the cached plans
+        if seq is not None:
+            self._alloc(seq)
+
+    def _alloc(self, seq):
+        if ceil_div(seq, TILE) != self.n_blocks:
+            raise ShapeError(f"seq {seq} gives {ceil_div(seq, TILE)} blocks, cache has {self.n_blocks}")
+        self.seq = int(seq)
+        self.stacks = torch.zeros(self.order + 1, self.seq, self.heads * TILE, dtype=torch.bfloat16,
+                                  device=self.device)
+
+    def ensure(self, seq):
+        if self.stacks is None:
+            self._alloc(seq)
+        elif seq != self.seq:
+            raise ShapeError(f"tile rows {seq} != cached {self.seq}")
+
+    def push(self, o, select=None, stream=None):
+        """Push fresh outputs o [seq, heads, 128] into every (selected) entry."""
+        o = check_bsd(o, "o", heads=self.heads)
+        self.ensure(o.shape[0])
+        sel = None
+        if select is not None:
+            sel = torch.as_tensor(select, dtype=torch.uint8).to(self.device).contiguous()
+            if tuple(sel.shape) != (self.heads, self.n_blocks):
+                raise ShapeError(f"select shape {tuple(sel.shape)} != {(self.heads, self.n_blocks)}")
+        _lib.call("fo_cache_push", o.data_ptr(), self.stacks.data_ptr(), self.valid.data_ptr(),
+                  self.seq, self.heads, TILE, self.n_blocks, self.order, _lib.ptr(sel),
+                  stream_ptr(stream))
+        self.version += 1
+        self._sel_keep = sel  # keep alive until the launch retires
+
+    def update(self, head, block, o_new):
+        """Reference signature (attention.py:128-131): push one tile. o_new is
+        the tile [rows, 128]; accepted from numpy or torch."""
+        tile = torch.as_tensor(np.asarray(o_new, dtype=np.float32) if not isinstance(o_new, torch.Tensor)
+                               else o_new)
+        if tile.dim() != 2 or tile.shape[1] != TILE:
+            raise ShapeError(f"tile shape {tuple(tile.shape)}; head_dim must be {TILE}")
+        if self.stacks is None:
+            raise ShapeError("allocate the cache with seq= before per-tile updates")
+        r0 = block * TILE
+        rows = min(TILE, self.seq - r0)
+        if tile.shape[0] != rows:
+            raise ShapeError(f"tile shape {tuple(tile.shape)} != cached ({rows}, {TILE})")
+        full = torch.zeros(self.seq, self.heads, TILE, dtype=torch.bfloat16, device=self.device)
+        full[r0:r0 + rows, head] = tile.to(self.device, torch.bfloat16)
+        sel = np.zeros((self.heads, self.n_blocks), np.uint8)
+        sel[head, block] = 1
+        self.push(full, select=sel)
+        torch.cuda.current_stream().synchronize()
+
+    def valid_orders(self, head, block):
+        return int(self.valid[head, block].item())
+
+    def entry(self, head, block):
+        if self.valid_orders(head, block) < 1:
+            return None
+        r0 = block * TILE
+        rows = min(TILE, self.seq - r0)
+        st = self.stacks[:, r0:r0 + rows, head * TILE:(head + 1) * TILE].float().cpu().numpy()
+        return CacheEntry(diff_stack=st, valid_orders=self.valid_orders(head, block))
+
+
+# ---------------------------------------------------------------------------
+def _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d, b_q, b_k,
+                      mode, counters, fill):
+    """Reference per-head signature: numpy [n, d] in, numpy fp32 out."""
+    q, k, v = (torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32)) for a in (q, k, v))
+    if q.dim() != 2:
+        raise ShapeError(f"q: expected a 2-D matrix, got shape {tuple(q.shape)}")
+    if q.shape[1] != TILE:
+        raise ParameterError(f"the B200 engine is built for head_dim {TILE}, got {q.shape[1]}")
+    dev = "cuda"
+    qd, kd, vd = (a.to(dev, torch.bfloat16).unsqueeze(1) for a in (q, k, v))
+    sym = symbols if isinstance(symbols, DeviceSymbols) else DeviceSymbols.from_buffers([symbols])
+    sub = None
+    if cache is not None:
+        sub = FeatureCache(1, cache.n_blocks, cache.order, seq=cache.seq)
+        sub.valid.copy_(cache.valid[head:head + 1])
+        if cache.stacks is not None:
+            sub.stacks.copy_(cache.stacks[:, :, head * TILE:(head + 1) * TILE])
+    out = torch.full_like(qd, float(fill), dtype=torch.bfloat16)
+    res = sparse_attention(qd, kd, vd, sym, sub, None, elapsed_k, interval_n, order_d, b_q=b_q,
+                           b_k=b_k, mode=mode, counters=counters, out=out)
+    arr = res[:, 0].float().cpu().numpy()
+    if fill is not None and np.isnan(fill):
+        # rows never written keep the caller's placeholder exactly
+        active, _ = sym.decoded()
+        rows = np.repeat(active[0].cpu().numpy().astype(bool), TILE)[: arr.shape[0]]
+        if mode == "bias":
+            arr[~rows] = np.nan
+    return arr
+
+
+def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d, *, b_q=TILE,
+                     b_k=TILE, mode="materialize", counters=None, backend=None, fill=0.0, out=None,
+                     stream=None, status=None, check=True):
+    """Symbol-guided attention for every head of a layer (attention.py:150-221).
+
+    q, k, v: bf16 [seq, heads, 128] on the GPU. symbols: DeviceSymbols.
+    cache: FeatureCache or None. mode="bias" leaves cached tiles untouched in
+    `out` (pre-filled with `fill` when `out` is not given); mode="materialize"
+    writes their forecast. Returns out [seq, heads, 128] bf16.
+    check=False defers the device contract checks (errors stay latched in the
+    status word) so the call never synchronises.
+    """
+    if backend is not None and getattr(backend, "NAME", "b200") != "b200":
+        raise ParameterError("this engine runs only its sm_100a kernels")
+    if mode not in ("materialize", "bias"):
+        raise ParameterError(f"unknown mode {mode!r}")
+    if b_q != TILE or b_k != TILE:
+        raise ParameterError(f"the sm_100a kernels tile blocks of {TILE} tokens (b_q=b_k={TILE})")
+    if isinstance(q, np.ndarray) or isinstance(symbols, SymbolBuffer):
+        return _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d,
+                                 b_q, b_k, mode, counters, fill)
+    require_cuda()
+    q = check_bsd(q, "q")
+    seq, heads = q.shape[0], q.shape[1]
+    k = check_bsd(k, "k", seq, heads)
+    v = check_bsd(v, "v", seq, heads)
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda:
+            raise ParameterError(f"{name}: expected a CUDA bf16 tensor")
+    t_q = ceil_div(seq, TILE)
+    if (symbols.rows, symbols.cols) != (t_q, t_q):
+        raise ShapeError(f"symbols dimensioned {symbols.rows}x{symbols.cols}, expected {t_q}x{t_q}")
+    if symbols.heads != heads:
+        raise ShapeError(f"symbols for {symbols.heads} heads, q has {heads}")
+    if mode == "materialize":
+        check_elapsed(elapsed_k, interval_n)
+    st = status or Status.default()
+    if cache is not None:
+        if (cache.heads, cache.n_blocks) != (heads, t_q):
+            raise ShapeError("feature cache geometry does not match q")
+        valid, vver = cache.valid, cache.version
+    else:
+        # no cache at all: any cached block is a cold-cache StateError
+        valid, vver = _zeros_valid(heads, t_q, q.device), -1
+    plan = symbols.plan(valid=valid, valid_version=vver, order_d=order_d, status=st,
+                        stream=stream, check=check)
+    if out is None:
+        out = torch.full((seq, heads, TILE), float(fill) if fill is not None else 0.0,
+                         dtype=torch.bfloat16, device=q.device)
+    pairs = torch.zeros(heads, dtype=torch.int64, device=q.device) if counters is not None else None
+    _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads, TILE,
+              symbols.s_s.data_ptr(), symbols.rows, symbols.cols, symbols.pool_n, plan.ptr(),
+              1.0 / math.sqrt(TILE), 0, out.data_ptr(), None, None, order_d, _lib.ptr(pairs),
+              st.ptr(), stream_ptr(stream))
+    if mode == "materialize":
+        n_orders = order_d + 1
+        coef = ctypes_floats(forecast_coefficients(elapsed_k, interval_n, n_orders))
+        _lib.call("fo_forecast_materialize", cache.stacks.data_ptr(), seq, heads, TILE, t_q,
+                  order_d, plan.ptr(), cache.valid.data_ptr(), ctypes.addressof(coef),
+                  out.data_ptr(),
+                  stream_ptr(stream))
+    if check:
+        st.check("sparse_attention")
+    if counters is not None:
+        counters.pairs_total += heads * t_q * t_q
+        counters.pairs_computed += int(pairs.sum().item())
+    return out
+
+
+def dense_attention_update(q, k, v, cache, *, out=None, counters=None, stream=None, status=None,
+                           check=True):
+    """Update-step attention (pipeline.py:268-278): dense over every pair, and
+    the epilogue pushes each fresh tile into the cache's difference stacks in
+    place (K2u) — no separate cache pass."""
+    require_cuda()
+    q = check_bsd(q, "q")
+    seq, heads = q.shape[0], q.shape[1]
+    k = check_bsd(k, "k", seq, heads)
+    v = check_bsd(v, "v", seq, heads)
+    t_q = ceil_div(seq, TILE)
+    if cache is not None:
+        if (cache.heads, cache.n_blocks) != (heads, t_q):
+            raise ShapeError("feature cache geometry does not match q")
+        cache.ensure(seq)
+    st = status or Status.default()
+    plan = _dense_plan(heads, t_q, q.device, st, stream)
+    if out is None:
+        out = torch.empty(seq, heads, TILE, dtype=torch.bfloat16, device=q.device)
+    pairs = torch.zeros(heads, dtype=torch.int64, device=q.device) if counters is not None else None
+    _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads, TILE,
+              plan.sym.s_s.data_ptr(), t_q, t_q, 1, plan.ptr(), 1.0 / math.sqrt(TILE),
+              1 if cache is not None else 0,
+              out.data_ptr(), None if cache is None else cache.stacks.data_ptr(),
+              None if cache is None else cache.valid.data_ptr(),
+              0 if cache is None else cache.order, _lib.ptr(pairs), st.ptr(), stream_ptr(stream))
+    if cache is not None:
+        cache.version += 1
+    if check:
+        st.check("dense_attention_update")
+    if counters is not None:
+        counters.pairs_total += heads * t_q * t_q
+        counters.pairs_computed += int(pairs.sum().item())
+    return out
+
+
+# ---------------------------------------------------------------------------
+_DENSE = {}
+_ZEROS = {}
+
+
+def _zeros_valid(heads, t_q, device):
+    key = (heads, t_q, str(device))
+    if key not in _ZEROS:
+        _ZEROS[key] = torch.zeros(heads, t_q, dtype=torch.int32, device=device)
+    return _ZEROS[key]
+
+
+def _dense_plan(heads, t_q, device, status, stream):
+    """Plan with every (head, block) active and every key block (update step)."""
+    key = (heads, t_q, str(device))
+    pl = _DENSE.get(key)
+    if pl is None:
+        from .symbols import encode_symbols
+
+        sym = encode_symbols(torch.ones(heads, t_q, dtype=torch.uint8, device=device),
+                             torch.ones(heads, t_q, t_q, dtype=torch.uint8, device=device), 1)
+        pl = sym.plan(dense=True, status=status, stream=stream)
+        pl.sym = sym
+        _DENSE[key] = pl
+    return pl
+
+
+def ctypes_floats(arr):
+    a = np.zeros(4, np.float32)
+    a[: len(arr)] = arr
+    return (ctypes.c_float * 4)(*a.tolist())

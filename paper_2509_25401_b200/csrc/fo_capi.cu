@@ -1,0 +1,339 @@
+// C ABI (include/flashomni_b200.h): argument validation, TMA descriptor
+// construction and kernel launches. No allocation, no synchronisation.
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/flashomni_b200.h"
+#include "fo_internal.cuh"
+
+using namespace fo;
+
+namespace {
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return FO_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] map, box = 64 columns (128 B) x box_rows, SW128
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+             const char* name) {
+  auto fn = encode_fn();
+  if (!fn) return fail(FO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(FO_ERR_PARAM, "%s: base address not 16-byte aligned", name);
+  if ((cols * 2) % 16 != 0) return fail(FO_ERR_SHAPE, "%s: row pitch not a multiple of 16 B", name);
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FO_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed (%d)", name, (int)r);
+  return FO_OK;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+PlanView plan_view(const void* ws, int H, int rows) {
+  PlanView pv;
+  plan_layout(H, rows, reinterpret_cast<char*>(const_cast<void*>(ws)), &pv);
+  return pv;
+}
+
+int check_symbol_dims(int heads, int rows, int cols, int pool_n) {
+  if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64], got %d", heads);
+  if (rows < 1 || cols < 1) return fail(FO_ERR_SHAPE, "symbol grid %dx%d is empty", rows, cols);
+  if (rows >= (1 << 20)) return fail(FO_ERR_PARAM, "too many query blocks (%d)", rows);
+  if (pool_n < 1) return fail(FO_ERR_CONSISTENCY, "pool_n must be >= 1, got %d", pool_n);
+  return FO_OK;
+}
+
+int check_head_dim(int head_dim) {
+  if (head_dim != kTile)
+    return fail(FO_ERR_PARAM, "B200 kernels are built for head_dim = %d, got %d", kTile, head_dim);
+  return FO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fo_abi_version(void) { return 1; }
+const char* fo_last_error(void) { return g_err; }
+int fo_num_sms(void) { return num_sms(); }
+
+size_t fo_plan_workspace_bytes(int heads, int rows) { return plan_layout(heads, rows, nullptr, nullptr); }
+
+void fo_plan_offsets(int heads, int rows, size_t offsets[6]) {
+  PlanView pv;
+  plan_layout(heads, rows, nullptr, &pv);
+  offsets[0] = reinterpret_cast<size_t>(pv.counts);
+  offsets[1] = reinterpret_cast<size_t>(pv.items);
+  offsets[2] = reinterpret_cast<size_t>(pv.gq_items);
+  offsets[3] = reinterpret_cast<size_t>(pv.hmask);
+  offsets[4] = reinterpret_cast<size_t>(pv.orders);
+  offsets[5] = reinterpret_cast<size_t>(pv.pairs_pred);
+}
+
+int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int heads, int rows,
+                      int cols, int pool_n, uint8_t* s_c, uint8_t* s_s, uint32_t* status,
+                      void* stream) {
+  int rc = check_symbol_dims(heads, rows, cols, pool_n);
+  if (rc) return rc;
+  const int comp_rows = ceil_div_d(rows, pool_n);
+  const long long warps = (long long)heads * (comp_rows + 1);
+  const int threads = 256;
+  const long long blocks = (warps * 32 + threads - 1) / threads;
+  encode_symbols_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      cache_bits, skip_bits, heads, rows, cols, pool_n, s_c, s_s, status);
+  return check_launch("encode_symbols");
+}
+
+int fo_decode_symbols(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols,
+                      int pool_n, uint8_t* active, uint8_t* pair_bits, void* stream) {
+  int rc = check_symbol_dims(heads, rows, cols, pool_n);
+  if (rc) return rc;
+  const long long total = (long long)heads * rows * cols;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  decode_symbols_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols,
+                                                                  pool_n, active, pair_bits);
+  return check_launch("decode_symbols");
+}
+
+int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols, int pool_n,
+            int dense, const int32_t* valid, int order_d, void* plan_ws, uint32_t* status,
+            void* stream) {
+  int rc = check_symbol_dims(heads, rows, cols, pool_n);
+  if (rc) return rc;
+  if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  PlanView pv = plan_view(plan_ws, heads, rows);
+  const size_t smem = (size_t)(2 * (cols + 2) + 1024) * sizeof(int);
+  if (smem > 200 * 1024) return fail(FO_ERR_PARAM, "too many key blocks (%d)", cols);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
+                                                       valid, order_d, pv, status);
+  return check_launch("plan");
+}
+
+int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, int heads,
+                        int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                        const void* plan_ws, float scale, int update_mode, void* out, void* cache,
+                        int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
+                        void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  rc = check_symbol_dims(heads, rows, cols, pool_n);
+  if (rc) return rc;
+  if (seq < 1) return fail(FO_ERR_SHAPE, "empty sequence");
+  const int t = ceil_div_d(seq, kTile);
+  if (rows != t || cols != t)
+    return fail(FO_ERR_SHAPE, "symbols dimensioned %dx%d, expected %dx%d", rows, cols, t, t);
+  if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3], got %d", order_d);
+  if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  CUtensorMap qm, km, vm;
+  const uint64_t HD = (uint64_t)heads * kTile;
+  if ((rc = make_map(&qm, q, seq, HD, kTile, "q"))) return rc;
+  if ((rc = make_map(&km, k, seq, HD, kTile, "k"))) return rc;
+  if ((rc = make_map(&vm, v, seq, HD, kTile, "v"))) return rc;
+  PlanView pv = plan_view(plan_ws, heads, rows);
+  AttnParams p;
+  p.S = seq;
+  p.H = heads;
+  p.t_q = rows;
+  p.t_kv = cols;
+  p.pool_n = pool_n;
+  p.comp_rows = ceil_div_d(rows, pool_n);
+  p.row_stride = ceil_div_d(ceil_div_d(cols, pool_n), 8);
+  p.dense = update_mode ? 1 : 0;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.s_s = s_s;
+  p.items = pv.items;
+  p.n_items = pv.counts;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.cache = update_mode ? static_cast<__nv_bfloat16*>(cache) : nullptr;
+  p.valid = update_mode ? valid : nullptr;
+  p.order_d = order_d;
+  p.pairs = reinterpret_cast<long long*>(pairs);
+  p.status = status;
+  if (!update_mode && !s_s) return fail(FO_ERR_PARAM, "s_s is NULL");
+  launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
+  return check_launch("sparse_attention");
+}
+
+int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim, int rows,
+                            int order_d, const void* plan_ws, const int32_t* valid,
+                            const float* coef, void* out, void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
+  if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
+  float c[4] = {0, 0, 0, 0};
+  for (int d = 0; d <= order_d; ++d) c[d] = coef[d];
+  PlanView pv = plan_view(plan_ws, heads, rows);
+  launch_forecast_materialize(static_cast<const __nv_bfloat16*>(cache), seq, heads, rows, order_d,
+                              pv.hmask, valid, c, static_cast<__nv_bfloat16*>(out),
+                              (cudaStream_t)stream);
+  return check_launch("forecast_materialize");
+}
+
+int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,
+                  int rows, int order_d, const uint8_t* select, void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
+  if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
+  launch_cache_push(static_cast<const __nv_bfloat16*>(o), static_cast<__nv_bfloat16*>(cache), valid,
+                    seq, heads, rows, order_d, select, (cudaStream_t)stream);
+  return check_launch("cache_push");
+}
+
+int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, int head_dim,
+              const float* norm_w, const float* rope_cos, const float* rope_sin, float eps,
+              const void* plan_ws, int dense, void* q_out, void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (d_model % 64 != 0 || d_model < 64) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 64");
+  if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64]");
+  if (!dense && !plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  CUtensorMap xm, wm;
+  if ((rc = make_map(&xm, x, seq, d_model, 128, "x"))) return rc;
+  if ((rc = make_map(&wm, w_qt, (uint64_t)heads * kTile, d_model, 128, "w_q"))) return rc;
+  const int t_q = ceil_div_d(seq, kTile);
+  GemmQParams p;
+  p.S = seq;
+  p.dm = d_model;
+  p.H = heads;
+  p.t_q = t_q;
+  p.dense = dense;
+  if (plan_ws) {
+    PlanView pv = plan_view(plan_ws, heads, t_q);
+    p.gq_items = pv.gq_items;
+    p.n_gq = pv.counts + 1;
+  } else {
+    p.gq_items = nullptr;
+    p.n_gq = nullptr;
+  }
+  p.norm_w = norm_w;
+  p.rope_cos = rope_cos;
+  p.rope_sin = rope_sin;
+  p.eps = eps;
+  p.q = static_cast<__nv_bfloat16*>(q_out);
+  launch_gemm_q(xm, wm, p, num_sms(), (cudaStream_t)stream);
+  return check_launch("gemm_q");
+}
+
+static int gemm_o_common(const void* o, const void* cache, const void* w_outt, int seq, int heads,
+                         int head_dim, int d_model, int order_d, const void* plan_ws,
+                         GemmOParams& p, CUtensorMap& am, CUtensorMap& cm, CUtensorMap& wm) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (d_model % 128 != 0) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 128");
+  if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64]");
+  if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
+  if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  const uint64_t HD = (uint64_t)heads * kTile;
+  if ((rc = make_map(&am, o, seq, HD, 128, "o"))) return rc;
+  if ((rc = make_map(&cm, cache ? cache : o, cache ? (uint64_t)(order_d + 1) * seq : seq, HD, 128,
+                     "cache")))
+    return rc;
+  if ((rc = make_map(&wm, w_outt, d_model, HD, 128, "w_out"))) return rc;
+  const int t_q = ceil_div_d(seq, kTile);
+  PlanView pv = plan_view(plan_ws, heads, t_q);
+  p.S = seq;
+  p.dm = d_model;
+  p.H = heads;
+  p.t_q = t_q;
+  p.order_d = order_d;
+  p.hmask = pv.hmask;
+  p.orders = pv.orders;
+  for (int d = 0; d < 4; ++d) p.coef[d] = 0.f;
+  p.status = nullptr;
+  return FO_OK;
+}
+
+int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int seq, int heads,
+                     int head_dim, int d_model, int order_d, const void* plan_ws, void* out,
+                     void* bias, uint32_t* status, void* stream) {
+  GemmOParams p;
+  CUtensorMap am, cm, wm;
+  int rc = gemm_o_common(o, cache, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p, am,
+                         cm, wm);
+  if (rc) return rc;
+  if (order_d > 0 && !cache) return fail(FO_ERR_PARAM, "order_d > 0 needs the diff-stack cache");
+  p.update = 1;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.bias = static_cast<__nv_bfloat16*>(bias);
+  p.status = status;
+  launch_gemm_o(am, cm, wm, p, num_sms(), (cudaStream_t)stream);
+  return check_launch("gemm_o_update");
+}
+
+int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, const int32_t* orders,
+                       int seq, int heads, int head_dim, int d_model, int order_d,
+                       const float* coef, const void* plan_ws, void* out, void* stream) {
+  GemmOParams p;
+  CUtensorMap am, cm, wm;
+  int rc = gemm_o_common(o, nullptr, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p,
+                         am, cm, wm);
+  if (rc) return rc;
+  if (!orders) return fail(FO_ERR_STATE, "dispatch projection requires the update-step bias");
+  p.update = 0;
+  p.orders = orders;
+  for (int d = 0; d <= order_d; ++d) p.coef[d] = coef[d];
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.bias = static_cast<__nv_bfloat16*>(const_cast<void*>(bias));
+  launch_gemm_o(am, cm, wm, p, num_sms(), (cudaStream_t)stream);
+  return check_launch("gemm_o_dispatch");
+}
+
+int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
+                          int pool_n, uint32_t* status, void* stream) {
+  int rc = check_symbol_dims(heads, rows, 1, pool_n);
+  if (rc) return rc;
+  const int total = heads * rows;
+  compare_active_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(s_c_a, s_c_b, heads,
+                                                                              rows, pool_n, status);
+  return check_launch("check_active_match");
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// Bandwidth-bound helpers around the tensor-core kernels.
+//
+// forecast_materialize: OP_reuse for mode="materialize" (reference
+//   attention.py:96-113,212-216): cached query tiles are written as
+//   sum_d c_d * diff_stack[d] into the attention output.
+// cache_push: FeatureCache.update for an arbitrary set of (head, block) entries
+//   (attention.py:71-85,128-131), the standalone form of the push the
+//   update-mode attention epilogue performs.
+// Both are HBM-bound; one CTA per (head, block) tile, 16-byte accesses.
+#include "fo_internal.cuh"
+
+namespace fo {
+
+__global__ void forecast_materialize_kernel(const __nv_bfloat16* __restrict__ cache, int S, int H,
+                                            int t_q, int order_d,
+                                            const unsigned long long* __restrict__ hmask,
+                                            const int32_t* __restrict__ valid, float c0, float c1,
+                                            float c2, float c3, __nv_bfloat16* __restrict__ out) {
+  const int tile = blockIdx.x;
+  const int h = tile / t_q, i = tile % t_q;
+  if ((hmask[i] >> h) & 1ull) return;  // computed tile, not forecast
+  const int n = min(order_d + 1, valid[(size_t)h * t_q + i]);
+  const float cf[4] = {c0, c1, c2, c3};
+  const size_t HD = (size_t)H * kTile;
+  const size_t SS = (size_t)S * HD;
+  const int rows = min(kTile, S - i * kTile);
+  for (int e = threadIdx.x; e < rows * 16; e += blockDim.x) {
+    const int rr = e >> 4, v = e & 15;
+    const size_t off = (size_t)(i * kTile + rr) * HD + (size_t)h * kTile + v * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int d = 0; d < n; ++d) {
+      const uint4 w = *reinterpret_cast<const uint4*>(cache + d * SS + off);
+      const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] = fmaf(cf[d], bf16lo(w4[q]), acc[2 * q]);
+        acc[2 * q + 1] = fmaf(cf[d], bf16hi(w4[q]), acc[2 * q + 1]);
+      }
+    }
+    uint4 pk;
+    pk.x = pack_bf16x2(acc[0], acc[1]);
+    pk.y = pack_bf16x2(acc[2], acc[3]);
+    pk.z = pack_bf16x2(acc[4], acc[5]);
+    pk.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(out + off) = pk;
+  }
+}
+
+__global__ void cache_push_kernel(const __nv_bfloat16* __restrict__ o, __nv_bfloat16* __restrict__ cache,
+                                  int32_t* __restrict__ valid, int S, int H, int t_q, int order_d,
+                                  const uint8_t* __restrict__ sel) {
+  const int tile = blockIdx.x;
+  const int h = tile / t_q, i = tile % t_q;
+  if (sel && !sel[(size_t)h * t_q + i]) return;
+  const int valid_old = valid[(size_t)h * t_q + i];
+  const int vn = min(valid_old + 1, order_d + 1);
+  const size_t HD = (size_t)H * kTile;
+  const size_t SS = (size_t)S * HD;
+  const int rows = min(kTile, S - i * kTile);
+  for (int e = threadIdx.x; e < rows * 16; e += blockDim.x) {
+    const int rr = e >> 4, v = e & 15;
+    const size_t off = (size_t)(i * kTile + rr) * HD + (size_t)h * kTile + v * 8;
+    const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
+    float cur[8] = {bf16lo(ov.x), bf16hi(ov.x), bf16lo(ov.y), bf16hi(ov.y),
+                    bf16lo(ov.z), bf16hi(ov.z), bf16lo(ov.w), bf16hi(ov.w)};
+    for (int d = 0; d <= order_d; ++d) {
+      uint4* slot = reinterpret_cast<uint4*>(cache + d * SS + off);
+      float nxt[8];
+      const bool live_next = d + 1 < vn;
+      if (live_next) {
+        const uint4 w = *slot;
+        const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          nxt[2 * q] = cur[2 * q] - bf16lo(w4[q]);
+          nxt[2 * q + 1] = cur[2 * q + 1] - bf16hi(w4[q]);
+        }
+      }
+      uint4 pk = make_uint4(0, 0, 0, 0);
+      if (d < vn) {
+        pk.x = pack_bf16x2(cur[0], cur[1]);
+        pk.y = pack_bf16x2(cur[2], cur[3]);
+        pk.z = pack_bf16x2(cur[4], cur[5]);
+        pk.w = pack_bf16x2(cur[6], cur[7]);
+      }
+      *slot = pk;
+      if (live_next) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) valid[(size_t)h * t_q + i] = vn;
+}
+
+void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,
+                                 const unsigned long long* hmask, const int32_t* valid,
+                                 const float* coef, __nv_bfloat16* out, cudaStream_t stream) {
+  forecast_materialize_kernel<<<H * t_q, 256, 0, stream>>>(cache, S, H, t_q, order_d, hmask, valid,
+                                                           coef[0], coef[1], coef[2], coef[3], out);
+}
+
+void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,
+                       int t_q, int order_d, const uint8_t* sel, cudaStream_t stream) {
+  cache_push_kernel<<<H * t_q, 256, 0, stream>>>(o, cache, valid, S, H, t_q, order_d, sel);
+}
+
+}  // namespace fo

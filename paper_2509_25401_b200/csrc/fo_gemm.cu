@@ -1,0 +1,453 @@
+// K3 GEMM-Q and K4/K5 GEMM-O on sm_100a (tcgen05 + TMEM + TMA, persistent).
+//
+// GEMM-Q (reference gemm.py:44-93 + tensor.py:68-109): output tile = (query
+// block i, head h), 128 x 128, so RMSNorm over the head dim and the
+// interleaved-pair RoPE are tile-local and run in the epilogue. Tiles whose
+// cache symbol is 0 are never scheduled (the plan lists only active tiles).
+//
+// GEMM-O (gemm.py:110-229): output tile = (block i, 128 columns of d_model);
+// the K loop walks heads, 128 K-columns each.
+//   dispatch: only heads active for block i are multiplied; the epilogue adds
+//             sum_d c_d * B_c[d] (the forecast of the cached-head bias).
+//   update:   job (i, n, d). d=0 accumulates cached heads into accumulator B and
+//             active heads into accumulator A in one K pass; B -> B_c[0],
+//             A + B -> out. d>=1 projects the cached heads' d-th difference
+//             stacks into B_c[d]. Every head is projected exactly once.
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..7 epilogue
+// (one accumulator row per thread). TMEM accumulators are double-buffered so
+// the epilogue of tile t overlaps the mainloop of tile t+1.
+#include "fo_internal.cuh"
+
+namespace fo {
+namespace gemm {
+constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int STAGES = 6;
+constexpr int NTHREADS = 256;
+
+struct Bars {
+  uint64_t full[STAGES], empty[STAGES];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
+
+__device__ __forceinline__ void init_bars(Bars* b) {
+  for (int s = 0; s < STAGES; ++s) {
+    mbar_init(&b->full[s], 1);
+    mbar_init(&b->empty[s], 1);
+  }
+  for (int a = 0; a < 2; ++a) {
+    mbar_init(&b->tfull[a], 1);
+    mbar_init(&b->tempty[a], 128);
+  }
+  fence_barrier_init();
+}
+
+// ring-buffer cursor
+struct Ring {
+  int s = 0, ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++s == STAGES) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+};
+
+// issue one BK=64 k-block: 4 x (128x128x16) MMAs
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_smem, uint32_t b_smem,
+                                           uint32_t idesc, bool acc_in) {
+#pragma unroll
+  for (int k = 0; k < BK / 16; ++k)
+    mma_bf16_ss(d_tmem, make_sdesc_sw128(a_smem + k * 32, 16, 1024),
+                make_sdesc_sw128(b_smem + k * 32, 16, 1024), idesc, (acc_in || k > 0) ? 1u : 0u);
+}
+
+template <int N>
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) asm volatile("" : "+r"(r[k]));
+}
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 pk;
+    pk.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+    pk.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+    pk.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+    pk.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+    d[q] = pk;
+  }
+}
+}  // namespace gemm
+
+// =============================================================================
+// GEMM-Q
+// =============================================================================
+__global__ void __launch_bounds__(gemm::NTHREADS, 1)
+    gemm_q_kernel(const __grid_constant__ CUtensorMap xm, const __grid_constant__ CUtensorMap wm,
+                  const GemmQParams p) {
+  using namespace gemm;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    init_bars(bars);
+    tma_prefetch_desc(&xm);
+    tma_prefetch_desc(&wm);
+  }
+  if (warp == 2) tmem_alloc<256>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+  const int n_jobs = p.dense ? p.t_q * p.H : *p.n_gq;
+  const int nkb = p.dm / BK;
+  auto job = [&](int w, int& h, int& i) {
+    if (p.dense) {
+      i = w / p.H;
+      h = w % p.H;
+    } else {
+      const int it = p.gq_items[w];
+      h = it >> 20;
+      i = it & 0xFFFFF;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Ring rg;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+        int h, i;
+        job(w, h, i);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+          uint8_t* st = smem + rg.s * STAGE_BYTES;
+          mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
+          tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
+          tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h * BN);
+          rg.next();
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      Ring rg;
+      int t = 0;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&bars->full[rg.s], rg.ph);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + rg.s * STAGE_BYTES);
+          mma_kblock(d, a, a + A_BYTES, idesc, kb > 0);
+          tc_commit(&bars->empty[rg.s]);
+          rg.next();
+        }
+        tc_commit(&bars->tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const size_t HD = (size_t)p.H * 128;
+    int t = 0;
+    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+      int h, i;
+      job(w, h, i);
+      const int acc = t & 1;
+      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t u[4][32];
+      const uint32_t ta = tbase + lane_off + acc * BN;
+      tmem_ld32(ta + 0, u[0]);
+      tmem_ld32(ta + 32, u[1]);
+      tmem_ld32(ta + 64, u[2]);
+      tmem_ld32(ta + 96, u[3]);
+      tmem_ld_wait();
+      gemm::reg_fence(u[0]);
+      gemm::reg_fence(u[1]);
+      gemm::reg_fence(u[2]);
+      gemm::reg_fence(u[3]);
+      tc_fence_before();
+      mbar_arrive(&bars->tempty[acc]);
+      const int row = i * BM + r;
+      __nv_bfloat16* dst = p.q + (size_t)row * HD + (size_t)h * 128;
+      if (row < p.S && !p.norm_w) {
+        // plain projection (V): no normalisation, no rotary encoding
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float o[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[c][k]);
+          gemm::store_bf16x32(dst + c * 32, o);
+        }
+      } else if (row < p.S) {
+        // RMSNorm (tensor.py:68-80): y * w / sqrt(mean(y^2) + eps)
+        float ss = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float v = __uint_as_float(u[c][k]);
+            ss = fmaf(v, v, ss);
+          }
+        const float inv = rsqrtf(ss * (1.f / 128.f) + p.eps);
+        const float* nw = p.norm_w + (size_t)h * 128;
+        const bool rope = p.rope_cos != nullptr;
+        const float* cs = rope ? p.rope_cos + (size_t)row * 64 : nullptr;
+        const float* sn = rope ? p.rope_sin + (size_t)row * 64 : nullptr;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float o[32];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            // interleaved-pair RoPE (tensor.py:83-109)
+            const int col = c * 32 + 2 * k;
+            const float e = __uint_as_float(u[c][2 * k]) * __ldg(nw + col) * inv;
+            const float od = __uint_as_float(u[c][2 * k + 1]) * __ldg(nw + col + 1) * inv;
+            if (rope) {
+              const float cv = __ldg(cs + col / 2), sv = __ldg(sn + col / 2);
+              o[2 * k] = e * cv - od * sv;
+              o[2 * k + 1] = e * sv + od * cv;
+            } else {
+              o[2 * k] = e;
+              o[2 * k + 1] = od;
+            }
+          }
+          gemm::store_bf16x32(dst + c * 32, o);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<256>(tbase);
+  }
+}
+
+// =============================================================================
+// GEMM-O (update: UPDATE=true, dispatch: UPDATE=false)
+// =============================================================================
+template <bool UPDATE>
+__global__ void __launch_bounds__(gemm::NTHREADS, 1)
+    gemm_o_kernel(const __grid_constant__ CUtensorMap am,  // o   [S, H*128]
+                  const __grid_constant__ CUtensorMap cm,  // diff stacks [(D+1)*S, H*128]
+                  const __grid_constant__ CUtensorMap wm,  // W_out^T [dm, H*128]
+                  const GemmOParams p) {
+  using namespace gemm;
+  constexpr int ACC_COLS = UPDATE ? 2 * BN : BN;  // update: accumulator A (active) + B (cached)
+  constexpr int TM_COLS = UPDATE ? 512 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    init_bars(bars);
+    tma_prefetch_desc(&am);
+    tma_prefetch_desc(&cm);
+    tma_prefetch_desc(&wm);
+  }
+  if (warp == 2) tmem_alloc<TM_COLS>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+  const int nbn = p.dm / BN;
+  const int nord = UPDATE ? p.order_d + 1 : 1;
+  const int n_jobs = p.t_q * nbn * nord;
+  const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
+  // job decode; returns false for update jobs with no work (d >= orders[i])
+  auto job = [&](int w, int& i, int& nb, int& d) -> bool {
+    d = w % nord;
+    const int rest = w / nord;
+    nb = rest % nbn;
+    i = rest / nbn;
+    return !(UPDATE && d > 0 && d >= p.orders[i]);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Ring rg;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+        int i, nb, d;
+        if (!job(w, i, nb, d)) continue;
+        const unsigned long long act = p.hmask[i];
+        const unsigned long long cached = all_heads & ~act;
+        // K order: [cached heads (update only)] then [active heads (d == 0 only)]
+        for (int pass = 0; pass < 2; ++pass) {
+          unsigned long long m;
+          if (pass == 0) m = UPDATE ? cached : 0ull;
+          else m = (d == 0) ? act : 0ull;
+          const CUtensorMap* src = (UPDATE && pass == 0 && d > 0) ? &cm : &am;
+          const int row0 = (UPDATE && pass == 0 && d > 0) ? d * p.S + i * BM : i * BM;
+          while (m) {
+            const int h = __ffsll(m) - 1;
+            m &= m - 1;
+            for (int kk = 0; kk < 2; ++kk) {
+              mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+              uint8_t* st = smem + rg.s * STAGE_BYTES;
+              mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
+              tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
+              tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * BN);
+              rg.next();
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      Ring rg;
+      int t = 0;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+        int i, nb, d;
+        if (!job(w, i, nb, d)) continue;
+        const int acc = t & 1;
+        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const unsigned long long act = p.hmask[i];
+        const unsigned long long cached = all_heads & ~act;
+        const uint32_t dA = tbase + acc * ACC_COLS;
+        const uint32_t dB = dA + (UPDATE ? BN : 0);
+        for (int pass = 0; pass < 2; ++pass) {
+          int nk;
+          if (pass == 0) nk = UPDATE ? 2 * __popcll(cached) : 0;
+          else nk = (d == 0) ? 2 * __popcll(act) : 0;
+          const uint32_t dst = (pass == 0) ? dB : dA;
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&bars->full[rg.s], rg.ph);
+            tc_fence_after();
+            const uint32_t a = smem_u32(smem + rg.s * STAGE_BYTES);
+            mma_kblock(dst, a, a + A_BYTES, idesc, kb > 0);
+            tc_commit(&bars->empty[rg.s]);
+            rg.next();
+          }
+        }
+        tc_commit(&bars->tfull[acc]);
+        ++t;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const size_t SD = (size_t)p.S * p.dm;
+    int t = 0;
+    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+      int i, nb, d;
+      if (!job(w, i, nb, d)) continue;
+      const int acc = t & 1;
+      const unsigned long long act = p.hmask[i];
+      const unsigned long long cached = all_heads & ~act;
+      const bool hasA = (d == 0) && act != 0ull;
+      const bool hasB = UPDATE && cached != 0ull;
+      const int no = UPDATE ? 0 : min(p.order_d + 1, p.orders[i]);
+      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int row = i * BM + r;
+      const bool row_ok = row < p.S;
+      const size_t obase = (size_t)row * p.dm + (size_t)nb * BN;
+      const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
+      const uint32_t tB = tA + (UPDATE ? BN : 0);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ua[32], ub[32];
+        if (hasA) tmem_ld32(tA + c * 32, ua);
+        if (UPDATE && hasB) tmem_ld32(tB + c * 32, ub);
+        tmem_ld_wait();
+        gemm::reg_fence(ua);
+        gemm::reg_fence(ub);
+        float o[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) o[k] = hasA ? __uint_as_float(ua[k]) : 0.f;
+        if (!row_ok) continue;
+        if (UPDATE) {
+          float b[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) b[k] = hasB ? __uint_as_float(ub[k]) : 0.f;
+          if (d == 0) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] += b[k];
+            gemm::store_bf16x32(p.out + obase + c * 32, o);
+          }
+          if (hasB && p.orders[i] > d) gemm::store_bf16x32(p.bias + d * SD + obase + c * 32, b);
+        } else {
+          for (int dd = 0; dd < no; ++dd) {
+            const uint4* bsrc = reinterpret_cast<const uint4*>(p.bias + dd * SD + obase + c * 32);
+            const float cf = p.coef[dd];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 bv = __ldg(bsrc + q);
+              const uint32_t w4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[q * 8 + 2 * e] = fmaf(cf, bf16lo(w4[e]), o[q * 8 + 2 * e]);
+                o[q * 8 + 2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[q * 8 + 2 * e + 1]);
+              }
+            }
+          }
+          gemm::store_bf16x32(p.out + obase + c * 32, o);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->tempty[acc]);
+      ++t;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TM_COLS>(tbase);
+  }
+}
+
+void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p, int grid,
+                   cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         gemm::SMEM_BYTES);
+    configured = true;
+  }
+  gemm_q_kernel<<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(xm, wm, p);
+}
+
+void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
+                   const GemmOParams& p, int grid, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_o_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         gemm::SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_o_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         gemm::SMEM_BYTES);
+    configured = true;
+  }
+  if (p.update)
+    gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, p);
+  else
+    gemm_o_kernel<false><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, p);
+}
+
+}  // namespace fo

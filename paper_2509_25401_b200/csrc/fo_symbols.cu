@@ -1,0 +1,249 @@
+// K1: sparse-symbol pack / decode and the per-layer schedule ("plan") kernels.
+//
+// Packing replaces the Python per-bit loops of reference symbols.py:39-81
+// (_compress_groups, _pack_row, encode_cache_mask, encode_skip_mask): one warp
+// per compressed row, lanes = compressed columns, __ballot_sync + __brev gives
+// the MSB-first bytes. Decoding (symbols.py:163-198) lives in fo_common.cuh and
+// is shared by every kernel prologue; fo_decode_symbols_kernel exposes it so the
+// decoded bits can be checked bit-for-bit against the reference.
+#include "fo_internal.cuh"
+
+namespace fo {
+
+// ---------------------------------------------------------------------------
+// encode
+// ---------------------------------------------------------------------------
+// One warp per (head, compressed row). Row -1 encodes s_c (the cache mask).
+__global__ void encode_symbols_kernel(const uint8_t* __restrict__ cache_bits,  // [H, rows]
+                                      const uint8_t* __restrict__ skip_bits,   // [H, rows, cols]
+                                      int H, int rows, int cols, int pool_n,
+                                      uint8_t* __restrict__ s_c,  // [H, sc_len]
+                                      uint8_t* __restrict__ s_s,  // [H, comp_rows, row_stride]
+                                      uint32_t* status) {
+  const int comp_rows = ceil_div_d(rows, pool_n), comp_cols = ceil_div_d(cols, pool_n);
+  const int sc_len = ceil_div_d(comp_rows, 8), row_stride = ceil_div_d(comp_cols, 8);
+  const int warps_per_head = comp_rows + 1;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= H * warps_per_head) return;
+  const int h = gw / warps_per_head;
+  const int r = gw % warps_per_head - 1;  // -1 -> s_c
+  if (r < 0) {
+    // cache mask: collapse groups along the only axis (symbols.py:39-53)
+    const uint8_t* cb = cache_bits + (size_t)h * rows;
+    for (int base = 0; base < comp_rows; base += 32) {
+      int c = base + lane;
+      uint32_t bit = 0;
+      if (c < comp_rows) {
+        int r0 = c * pool_n, r1 = min(r0 + pool_n, rows);
+        uint32_t v0 = cb[r0] != 0;
+        for (int rr = r0 + 1; rr < r1; ++rr)
+          if ((cb[rr] != 0) != v0) raise_status(status, ST_CONSISTENCY);
+        bit = v0;
+      }
+      uint32_t m = __brev(__ballot_sync(0xffffffffu, bit));
+      if (lane < 4) {
+        int byte = (base >> 3) + lane;
+        if (byte < sc_len) s_c[(size_t)h * sc_len + byte] = (uint8_t)(m >> (24 - 8 * lane));
+      }
+    }
+    return;
+  }
+  // skip mask row r: every pool_n x pool_n group must be uniform (symbols.py:73-81)
+  const uint8_t* sb = skip_bits + (size_t)h * rows * cols;
+  const int r0 = r * pool_n, r1 = min(r0 + pool_n, rows);
+  uint8_t* out = s_s + ((size_t)h * comp_rows + r) * row_stride;
+  for (int base = 0; base < comp_cols; base += 32) {
+    int c = base + lane;
+    uint32_t bit = 0;
+    if (c < comp_cols) {
+      int c0 = c * pool_n, c1 = min(c0 + pool_n, cols);
+      uint32_t v0 = sb[(size_t)r0 * cols + c0] != 0;
+      for (int rr = r0; rr < r1; ++rr)
+        for (int cc = c0; cc < c1; ++cc)
+          if ((sb[(size_t)rr * cols + cc] != 0) != v0) raise_status(status, ST_CONSISTENCY);
+      bit = v0;
+    }
+    uint32_t m = __brev(__ballot_sync(0xffffffffu, bit));
+    if (lane < 4) {
+      int byte = (base >> 3) + lane;
+      if (byte < row_stride) out[byte] = (uint8_t)(m >> (24 - 8 * lane));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decode (exposes the kernels' prologue decoders for bit-exact checks)
+// ---------------------------------------------------------------------------
+__global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s,
+                                      int H, int rows, int cols, int pool_n,
+                                      uint8_t* __restrict__ active,      // [H, rows]
+                                      uint8_t* __restrict__ pair_bits) {  // [H, rows, cols]
+  const int comp_rows = ceil_div_d(rows, pool_n), comp_cols = ceil_div_d(cols, pool_n);
+  const int sc_len = ceil_div_d(comp_rows, 8), row_stride = ceil_div_d(comp_cols, 8);
+  const size_t total = (size_t)H * rows * cols;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    int j = (int)(idx % cols);
+    int i = (int)((idx / cols) % rows);
+    int h = (int)(idx / ((size_t)cols * rows));
+    pair_bits[idx] = (uint8_t)decode_reduction(s_s + (size_t)h * comp_rows * row_stride, row_stride,
+                                               i, j, pool_n);
+    if (j == 0) active[(size_t)h * rows + i] = (uint8_t)decode_spatial(s_c + (size_t)h * sc_len, i, pool_n);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan: one CTA turns the symbols of a layer into the schedules the hot-path
+// kernels consume. Everything here is integer work on a few KB.
+// ---------------------------------------------------------------------------
+__device__ int row_popcount(const uint8_t* row, int comp_cols, int cols, int pool_n) {
+  int cnt = 0;
+  const int nbytes = ceil_div_d(comp_cols, 8);
+  for (int b = 0; b < nbytes; ++b) {
+    uint32_t byte = row[b];
+    int nvalid = min(8, comp_cols - b * 8);
+    byte &= (0xFFu << (8 - nvalid)) & 0xFFu;  // ignore padding bits (decode_run truncates)
+    if (pool_n == 1) {
+      cnt += __popc(byte);
+    } else {
+      while (byte) {
+        int k = __clz(byte) - 24;  // MSB-first bit index
+        byte &= ~(0x80u >> k);
+        int c = b * 8 + k;
+        cnt += min(pool_n, cols - c * pool_n);
+      }
+    }
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(1024, 1)
+plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
+            int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
+            PlanView pv, uint32_t* status) {
+  extern __shared__ int plan_smem[];
+  int* hist = plan_smem;        // [cols + 2]
+  int* offs = hist + cols + 2;  // [cols + 2]
+  int* scan = offs + cols + 2;  // [1024]
+  __shared__ unsigned long long s_pairs[64];
+  const int comp_rows = ceil_div_d(rows, pool_n), comp_cols = ceil_div_d(cols, pool_n);
+  const int sc_len = ceil_div_d(comp_rows, 8), row_stride = ceil_div_d(comp_cols, 8);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int total = H * rows;
+
+  for (int c = tid; c < cols + 2; c += nt) hist[c] = 0;
+  for (int h = tid; h < 64; h += nt) s_pairs[h] = 0;
+  __syncthreads();
+
+  auto is_active = [&](int h, int i) -> int {
+    return dense ? 1 : (int)decode_spatial(s_c + (size_t)h * sc_len, i, pool_n);
+  };
+  auto kv_count = [&](int h, int i) -> int {
+    if (dense) return cols;
+    return row_popcount(s_s + ((size_t)h * comp_rows + i / pool_n) * row_stride, comp_cols, cols,
+                        pool_n);
+  };
+
+  // pass 1: histogram of per-row KV counts, head masks, checks
+  for (int i = tid; i < rows; i += nt) {
+    unsigned long long m = 0;
+    int min_valid = 1 << 30;
+    bool any_cached = false;
+    for (int h = 0; h < H; ++h) {
+      int a = is_active(h, i);
+      if (a) {
+        m |= 1ull << h;
+      } else {
+        any_cached = true;
+        if (valid) min_valid = min(min_valid, valid[(size_t)h * rows + i]);
+      }
+    }
+    pv.hmask[i] = m;
+    // n_orders for the GEMM-O cached bias of block i (gemm.py:140-153)
+    int no = 0;
+    if (any_cached) {
+      no = valid ? min(order_d + 1, min_valid) : order_d + 1;
+      if (no < 1) raise_status(status, ST_STATE);
+    }
+    pv.orders[i] = no;
+  }
+  for (int idx = tid; idx < total; idx += nt) {
+    int h = idx / rows, i = idx % rows;
+    if (is_active(h, i)) {
+      int cnt = kv_count(h, i);
+      if (cnt == 0) {
+        // active query block with every key block skipped (pyref.py:43-46)
+        raise_status(status, ST_CONSISTENCY);
+      } else {
+        atomicAdd(&hist[cnt], 1);
+        atomicAdd(&s_pairs[h], (unsigned long long)cnt);
+      }
+    } else if (valid && valid[(size_t)h * rows + i] < 1) {
+      // cached tile with a cold cache (attention.py:208-211)
+      raise_status(status, ST_STATE);
+    }
+  }
+  __syncthreads();
+  // descending exclusive scan of the histogram (longest rows first)
+  if (tid == 0) {
+    int run = 0;
+    for (int c = cols; c >= 1; --c) {
+      offs[c] = run;
+      run += hist[c];
+    }
+    pv.counts[0] = run;  // attention items
+  }
+  for (int h = tid; h < H; h += nt) pv.pairs_pred[h] = (long long)s_pairs[h];
+  __syncthreads();
+  // pass 2: scatter attention items (sorted by KV count, descending)
+  for (int idx = tid; idx < total; idx += nt) {
+    int h = idx / rows, i = idx % rows;
+    if (is_active(h, i)) {
+      int cnt = kv_count(h, i);
+      if (cnt > 0) {
+        int pos = atomicAdd(&offs[cnt], 1);
+        pv.items[pos] = make_int2((h << 20) | i, cnt);
+      }
+    }
+  }
+  // pass 3: GEMM-Q tile list in (block, head) order: compaction via block scan
+  const int per = ceil_div_d(total, nt);
+  const int lo = min(total, tid * per), hi = min(total, lo + per);
+  int local = 0;
+  for (int idx = lo; idx < hi; ++idx) {
+    int i = idx / H, h = idx % H;
+    local += is_active(h, i);
+  }
+  scan[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    int v = tid >= off ? scan[tid - off] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int pos = scan[tid] - local;
+  for (int idx = lo; idx < hi; ++idx) {
+    int i = idx / H, h = idx % H;
+    if (is_active(h, i)) pv.gq_items[pos++] = (h << 20) | i;
+  }
+  if (tid == nt - 1) pv.counts[1] = scan[nt - 1];
+}
+
+// ---------------------------------------------------------------------------
+// stale-symbol check for GEMM-O dispatch (gemm.py:201-209): decoded active
+// heads of the dispatch symbols must equal those the bias was built under.
+// ---------------------------------------------------------------------------
+__global__ void compare_active_kernel(const uint8_t* __restrict__ s_c_a, const uint8_t* __restrict__ s_c_b,
+                                      int H, int rows, int pool_n, uint32_t* status) {
+  const int sc_len = ceil_div_d(ceil_div_d(rows, pool_n), 8);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < H * rows; idx += gridDim.x * blockDim.x) {
+    int h = idx / rows, i = idx % rows;
+    if (decode_spatial(s_c_a + (size_t)h * sc_len, i, pool_n) !=
+        decode_spatial(s_c_b + (size_t)h * sc_len, i, pool_n))
+      raise_status(status, ST_STATE);
+  }
+}
+
+}  // namespace fo

@@ -1,0 +1,124 @@
+"""One DiT attention layer on the GPU: the callers of the hot path.
+
+Mirrors reference pipeline.py:223-326. update_step refreshes the feature
+cache and the GEMM-O bias and computes the step densely; dispatch_step runs
+the sparse chain GEMM-Q -> sparse attention (mode="bias") -> GEMM-O dispatch
+against the governing update step's symbols. The update-step mask policy
+(policy.py) is not on the GPU yet, so update_step takes the next window's
+symbols from the caller.
+
+Multi-GPU: heads are sharded across ranks (shard_heads). GEMM-Q and K/V are
+column-parallel, attention and the cache are per head, GEMM-O is row-parallel
+and its partial outputs (each rank's heads, including each rank's partial
+cached bias) are summed by one all-reduce — exact by linearity of the
+projection and the forecast.
+"""
+
+from dataclasses import dataclass
+
+import torch
+
+from ._runtime import TILE, Status, as_device
+from .attention import FeatureCache, dense_attention_update, sparse_attention
+from .errors import ParameterError, StateError
+from .gemm import pack_w_out, pack_w_q, project_out_dispatch, project_out_update, project_q
+from .symbols import ceil_div
+
+
+@dataclass
+class LayerParams:
+    """Packed bf16 weights of one layer (reference LayerParams, pipeline.py:115-122)."""
+
+    w_q: object
+    w_k: object
+    w_v: object
+    q_norm: torch.Tensor
+    k_norm: torch.Tensor
+    w_out: object
+
+    @classmethod
+    def from_reference(cls, w_q, w_k, w_v, q_norm, k_norm, w_out, heads=None):
+        """Pack reference-layout weights ([H, dm, D] / [H, D, dm], any device).
+        heads: optional index list to keep (head-sharded rank)."""
+        def sel(a):
+            a = torch.as_tensor(a)
+            return a if heads is None else a[list(heads)]
+        return cls(w_q=pack_w_q(sel(w_q)), w_k=pack_w_q(sel(w_k)), w_v=pack_w_q(sel(w_v)),
+                   q_norm=as_device(sel(q_norm), torch.float32, "q_norm"),
+                   k_norm=as_device(sel(k_norm), torch.float32, "k_norm"),
+                   w_out=pack_w_out(sel(w_out)))
+
+    @property
+    def heads(self):
+        return self.w_q.heads
+
+
+@dataclass
+class LayerState:
+    params: LayerParams
+    cache: FeatureCache
+    symbols: object = None
+    bias: object = None
+
+
+def shard_heads(heads, world, rank):
+    """Contiguous head range owned by `rank` (heads must divide evenly)."""
+    if heads % world:
+        raise ParameterError(f"{heads} heads do not shard evenly over {world} ranks")
+    per = heads // world
+    return list(range(rank * per, (rank + 1) * per))
+
+
+def project_kv(x, params, *, eps=1e-6, k_out=None, v_out=None, stream=None):
+    """Dense K (RMS norm + RoPE) and V projections (pipeline.py:223-234) on the
+    GEMM-Q kernel in dense mode."""
+    k = project_q(x, params.w_k, params.k_norm, None, "update", eps=eps, out=k_out, fill=None,
+                  stream=stream)
+    v = project_q(x, params.w_v, None, None, "update", rope=False, out=v_out, fill=None,
+                  stream=stream)
+    return k, v
+
+
+def _allreduce(out, group):
+    if group is not None:
+        import torch.distributed as dist
+
+        dist.all_reduce(out, group=group)
+    return out
+
+
+def update_step(state, x, symbols_next, order_d, *, group=None, check=True):
+    """Refresh cache and bias; compute the step densely (pipeline.py:244-288)."""
+    x = as_device(x, torch.bfloat16, "x")
+    p = state.params
+    q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None)
+    k, v = project_kv(x, p)
+    o = dense_attention_update(q, k, v, state.cache, check=check)
+    out, bias = project_out_update(o, p.w_out, symbols_next, state.cache, order_d, check=check)
+    state.symbols = symbols_next
+    state.bias = bias
+    return _allreduce(out, group)
+
+
+def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check=True, fill=None,
+                  bufs=None):
+    """Sparse execution against the governing symbols (pipeline.py:291-326).
+    bufs: optional dict of preallocated q/k/v/o/out tensors (graph capture)."""
+    if state.symbols is None or state.bias is None:
+        raise StateError("dispatch step before any update step")
+    x = as_device(x, torch.bfloat16, "x")
+    p = state.params
+    b = bufs or {}
+    q = project_q(x, p.w_q, p.q_norm, state.symbols, "dispatch", fill=fill, out=b.get("q"),
+                  check=check)
+    k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"))
+    o = sparse_attention(q, k, v, state.symbols, state.cache, None, elapsed_k, interval_n, order_d,
+                         mode="bias", fill=fill, out=b.get("o"), check=check)
+    out = project_out_dispatch(o, p.w_out, state.symbols, state.bias, elapsed_k, interval_n,
+                               order_d, out=b.get("out"), check=check)
+    return _allreduce(out, group)
+
+
+def new_layer_state(params, seq, order_d):
+    t_q = ceil_div(seq, TILE)
+    return LayerState(params=params, cache=FeatureCache(params.heads, t_q, order_d, seq=seq))
