@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""FlashOmni B200 hot-path benchmark (BASELINE.json metric).
+
+A step = one dispatch step of the sparse hot path of one HunyuanVideo DiT
+attention layer (C4: 33,024 tokens = 258 blocks of 128, 24 heads x 128,
+d_model 3072): GEMM-Q (cached tiles dropped) -> sparse attention (cached
+q-blocks and masked KV blocks skipped) -> GEMM-O dispatch (cached-head
+K-blocks dropped, forecast bias added). Symbols are random 8-bit symbols in
+the reference's random_masks rule (verify.py:29-44): 25% cached q-blocks, 50%
+KV blocks skipped in active rows (62.5% pair sparsity). Inputs are resident in
+HBM and larger than L2 (x, q, k, v, o are 203 MB each), so no flush is needed.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun): heads are sharded over ranks (C5): each rank runs its heads
+and GEMM-O partial sums are all-reduced over NCCL inside the step.
+"""
+
+import argparse
+import json
+import os
+import pathlib
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sparse attn/GEMM-Q/GEMM-O ms & speedup vs sparsity ratio, Hunyuan 33K tokens"
+T = 128
+CONFIGS = {
+    "c4": dict(name="C4 HunyuanVideo attention layer, 33K tokens", seq=33024, heads=24, d_model=3072),
+    "c1": dict(name="C1 single DiT attention layer, 4096 tokens", seq=4096, heads=24, d_model=3072),
+    "c2": dict(name="C2 FLUX.1-dev joint attention, 4608 tokens", seq=4608, heads=24, d_model=3072),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--cached", type=float, default=0.25, help="cached q-block ratio")
+    ap.add_argument("--skip", type=float, default=0.5, help="KV block skip ratio in active rows")
+    ap.add_argument("--interval", type=int, default=6)
+    ap.add_argument("--order", type=int, default=1)
+    ap.add_argument("--elapsed", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also sweep sparsity (extra JSON key)")
+    return ap.parse_args()
+
+
+def random_masks(rng, heads, t, cached_ratio, skip_ratio):
+    """Vectorised verify.py:29-44 rule (pool_n = 1): cache density 1-cached,
+    pair density 1-skip, >= 1 computed pair per active row, cached rows empty."""
+    cache = rng.random((heads, t)) >= cached_ratio
+    skip = rng.random((heads, t, t)) >= skip_ratio
+    for h in range(heads):
+        if not cache[h].any():
+            cache[h, rng.integers(t)] = True
+    empty = cache & ~skip.any(axis=2)
+    hh, rr = np.nonzero(empty)
+    skip[hh, rr, rng.integers(t, size=hh.size)] = True
+    skip &= cache[:, :, None]
+    return cache, skip
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get(
+            "hbm_gbs", 6650.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port of the reference CPU path
+# ---------------------------------------------------------------------------
+def cpu_sample(cfg, cache_bits, skip_bits, seed, n_blocks=24):
+    """Time the reference CPU path (oracle port of pyref.py:14-48,
+    gemm.py:44-93,178-229; numpy + OpenBLAS on all host threads) on a bounded
+    sample — `n_blocks` active query blocks of head 0 for attention and
+    GEMM-Q, and the same row blocks (all heads) for GEMM-O dispatch — and scale
+    by exact work counts to one full layer step. Returns (ms, sample text)."""
+    import oracle
+
+    rng = np.random.default_rng(seed)
+    S, H, dm = cfg["seq"], cfg["heads"], cfg["d_model"]
+    t = S // T
+    q, k, v = (rng.standard_normal((S, T)).astype(np.float32) for _ in range(3))
+    blocks = np.flatnonzero(cache_bits[0])[:n_blocks]
+    act = np.zeros(t, np.uint8)
+    act[blocks] = 1
+    out = np.zeros((S, T), np.float32)
+    t0 = time.perf_counter()
+    pairs_s = oracle.masked_block_attention(q, k, v, act, skip_bits[0].astype(np.uint8), T, T,
+                                            1 / np.sqrt(T), out)
+    t_attn = time.perf_counter() - t0
+    pairs_all = int(sum(skip_bits[h][cache_bits[h]].sum() for h in range(H)))
+    x = rng.standard_normal((S, dm)).astype(np.float32)
+    wq = (rng.standard_normal((1, dm, T)) * dm ** -0.5).astype(np.float32)
+    nw = np.ones((1, T), np.float32)
+    sel = np.zeros((1, t), bool)
+    sel[0, blocks] = True
+    t0 = time.perf_counter()
+    oracle.project_q(x, wq, nw, sel, T)
+    t_q = time.perf_counter() - t0
+    rows_all = int(cache_bits.sum()) * T
+    # GEMM-O dispatch on the sample row blocks (all heads)
+    o = rng.standard_normal((H, len(blocks) * T, T)).astype(np.float32)
+    w_out = (rng.standard_normal((H, T, dm)) * T ** -0.5).astype(np.float32)
+    active = cache_bits[:, blocks].T
+    bias = [rng.standard_normal((2, T, dm)).astype(np.float32) for _ in blocks]
+    orders = np.where((~active).any(axis=1), 2, 0)
+    t0 = time.perf_counter()
+    oracle.project_out_dispatch(o, w_out, active, bias, orders, 1, 6, 1, T)
+    t_o = time.perf_counter() - t0
+    act_all = int(cache_bits.sum())
+    est = (t_attn * pairs_all / pairs_s + t_q * rows_all / (len(blocks) * T)
+           + t_o * act_all / max(int(active.sum()), 1))
+    sample = (f"{len(blocks)} active q-blocks of head 0 (attention {pairs_s} of {pairs_all} pairs, "
+              f"GEMM-Q), GEMM-O dispatch on those {len(blocks)} row blocks x {H} heads; "
+              f"scaled by exact pair / MAC counts to one full layer step")
+    return est * 1e3, sample, {"attn_ms": t_attn * pairs_all / pairs_s * 1e3,
+                               "gemm_q_ms": t_q * rows_all / (len(blocks) * T) * 1e3,
+                               "gemm_o_ms": t_o * act_all / max(int(active.sum()), 1) * 1e3}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    rng = np.random.default_rng(args.seed)
+    t = cfg["seq"] // T
+    cache_bits, skip_bits = random_masks(rng, cfg["heads"], t, args.cached, args.skip)
+    for _ in range(args.warmup):
+        cpu_sample(cfg, cache_bits, skip_bits, args.seed, n_blocks=8)
+    vals = []
+    for s in range(args.steps):
+        ms, sample, parts = cpu_sample(cfg, cache_bits, skip_bits, args.seed + s, n_blocks=8)
+        vals.append(ms)
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1) tensors, random symbols)",
+            "config": config_json(args, cfg, world, cache_bits, skip_bits),
+            "breakdown_ms": {k: round(x, 3) for k, x in parts.items()},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_threads(),
+                             "kind": "port", "sample": sample.replace("24 active", "8 active")},
+            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(args, cfg, world, cache_bits, skip_bits):
+    H, t = cfg["heads"], cfg["seq"] // T
+    computed = int(sum(skip_bits[h][cache_bits[h]].sum() for h in range(H)))
+    return {"workload": cfg["name"], "seq": cfg["seq"], "heads": H, "head_dim": T,
+            "d_model": cfg["d_model"], "b_q": T, "b_k": T, "pool_n": 1,
+            "cached_ratio": args.cached, "kv_skip_ratio": args.skip,
+            "pair_sparsity": round(1 - computed / (H * t * t), 4),
+            "interval_n": args.interval, "order_d": args.order, "elapsed_k": args.elapsed,
+            "symbols": "random (verify.py:29-44 rule), seed %d" % args.seed,
+            "parallelism": "heads/%d" % world if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (x/q/k/v/o 203 MB each), no flush"}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args, cfg, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_25401_b200 as fo
+    from paper_2509_25401_b200 import _lib
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    group = dist.group.WORLD if world > 1 else None
+    S, H, dm = cfg["seq"], cfg["heads"], cfg["d_model"]
+    t = S // T
+    rng = np.random.default_rng(args.seed)
+    cache_bits, skip_bits = random_masks(rng, H, t, args.cached, args.skip)
+    heads = fo.shard_heads(H, world, rank)
+    Hl = len(heads)
+    g = torch.Generator(device=dev).manual_seed(args.seed)
+
+    def randn(*shape, scale=1.0):
+        return torch.randn(*shape, device=dev, generator=g) * scale
+
+    # weights (reference init, pipeline.py:145-159), packed once
+    params = fo.LayerParams.from_reference(
+        randn(H, dm, T, scale=dm ** -0.5), randn(H, dm, T, scale=dm ** -0.5),
+        randn(H, dm, T, scale=dm ** -0.5), 1 + 0.05 * randn(H, T), 1 + 0.05 * randn(H, T),
+        randn(H, T, dm, scale=T ** -0.5), heads=heads)
+    x = randn(S, dm).bfloat16()
+    k, v = fo.project_kv(x, params)
+    sym = fo.encode_symbols(cache_bits[heads], skip_bits[heads], 1)
+    dense_sym = fo.encode_symbols(np.ones((Hl, t), bool), np.ones((Hl, t, t), bool), 1)
+    cache = fo.FeatureCache(Hl, t, args.order, seq=S)
+    for _ in range(args.order + 1):
+        cache.push(randn(S, Hl, T).bfloat16())
+    o_upd = randn(S, Hl, T).bfloat16()
+    _, bias = fo.project_out_update(o_upd, params.w_out, sym, cache, args.order)
+    _, bias_dense = fo.project_out_update(o_upd, params.w_out, dense_sym, cache, args.order)
+    q = torch.empty(S, Hl, T, dtype=torch.bfloat16, device=dev)
+    o = torch.empty_like(q)
+    out = torch.empty(S, dm, dtype=torch.bfloat16, device=dev)
+    torch.cuda.synchronize()
+
+    def step(sy, bs, ev=None):
+        if ev:
+            ev[0].record()
+        fo.project_q(x, params.w_q, params.q_norm, sy, "dispatch", out=q, fill=None, check=False)
+        if ev:
+            ev[1].record()
+        fo.sparse_attention(q, k, v, sy, cache, None, args.elapsed, args.interval, args.order,
+                            mode="bias", out=o, fill=None, check=False)
+        if ev:
+            ev[2].record()
+        fo.project_out_dispatch(o, params.w_out, sy, bs, args.elapsed, args.interval, args.order,
+                                out=out, check=False)
+        if group is not None:
+            dist.all_reduce(out, group=group)
+        if ev:
+            ev[3].record()
+
+    def timed(sy, bs, steps, warm, clocks=None):
+        for _ in range(warm):
+            step(sy, bs)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        _lib.reset_launch_count()
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            start.record()
+            for s in range(steps):
+                step(sy, bs, evs[s])
+            end.record()
+            torch.cuda.synchronize()
+        launches = _lib.launch_count()
+        if group is not None:
+            dist.barrier()
+        total = start.elapsed_time(end)
+        parts = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])]
+                          for e in evs]).mean(axis=0)
+        total_t = torch.tensor([total], device=dev)
+        if group is not None:
+            dist.all_reduce(total_t, op=dist.ReduceOp.MAX, group=group)
+        return total_t.item() / steps, parts, launches
+
+    # check once that the contract holds (errors are latched, not raised, while timing)
+    step(sym, bias)
+    fo._runtime.Status.default().check("bench warm-up")
+    clocks = Clocks(dev.index) if rank == 0 else None
+    ms, parts, launches = timed(sym, bias, args.steps, args.warmup, clocks)
+    fo._runtime.Status.default().check("bench timed region")
+    res = {"ms": ms, "parts": parts, "launches": launches}
+    if not args.no_dense:
+        dms, dparts, _ = timed(dense_sym, bias_dense, max(3, args.steps // 2), 2)
+        res.update(dense_ms=dms, dense_parts=dparts)
+
+    # e2e through the public API with host buffers: x H2D, dispatch_step, out D2H
+    e2e = None
+    if not args.no_e2e:
+        state = fo.LayerState(params=params, cache=cache, symbols=sym, bias=bias)
+        x_host = x.cpu().pin_memory()
+        out_host = torch.empty(S, dm, dtype=torch.bfloat16).pin_memory()
+        x_dev = torch.empty_like(x)
+        bufs = {"q": q, "k": torch.empty_like(q), "v": torch.empty_like(q), "o": o, "out": out}
+
+        def e2e_step():
+            x_dev.copy_(x_host, non_blocking=True)
+            r = fo.dispatch_step(state, x_dev, args.elapsed, args.interval, args.order, group=group,
+                                 check=False, bufs=bufs)
+            out_host.copy_(r, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        _lib.reset_launch_count()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        s1.record()
+        torch.cuda.synchronize()
+        e2e_launches = _lib.launch_count()
+        et = torch.tensor([s0.elapsed_time(s1) / args.steps], device=dev)
+        if group is not None:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX, group=group)
+        fo._runtime.Status.default().check("bench e2e")
+        e2e = {"value": round(et.item(), 3), "unit": "ms",
+               "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": out.numel() * 2,
+               "path": "pipeline.dispatch_step (GEMM-Q, K/V projection, sparse attention, "
+                       "GEMM-O dispatch) with pinned host x in / out back",
+               "gpu_launches_per_step": e2e_launches / args.steps}
+
+    if rank != 0:
+        return
+    # ---------------- roofline of the dominant kernel (sparse attention)
+    burst, sustained, hbm, src = peaks()
+    computed = int(sum(skip_bits[h][cache_bits[h]].sum() for h in heads))
+    attn_flops = 4.0 * T * T * T * computed
+    ach = attn_flops / (parts[1] * 1e-3) / 1e12
+    prof = ROOT / "profiles" / "ncu_r01_summary.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("attention", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    q_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
+    o_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (N(0,1) activations, reference-init weights, random 8-bit symbols)",
+        "config": config_json(args, cfg, world, cache_bits, skip_bits),
+        "breakdown_ms": {"gemm_q": round(parts[0], 4), "attention": round(parts[1], 4),
+                         "gemm_o_dispatch": round(parts[2], 4)},
+        "effective_tflops": {"gemm_q": round(q_flops / parts[0] / 1e9, 1),
+                             "attention": round(ach, 1),
+                             "gemm_o_dispatch": round(o_flops / parts[2] / 1e9, 1)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": sustained,
+                     "unit": "TFLOP/s", "frac": round(ach / sustained, 4), "traffic": traffic,
+                     "kernel": "sparse_attention_kernel", "peak_source": f"{src} bf16 sustained",
+                     "algorithmic_flops_per_launch": attn_flops},
+    }
+    if "dense_ms" in res:
+        dp = res["dense_parts"]
+        s_attn = 1 - computed / (Hl * t * t)
+        s_rows = 1 - int(cache_bits[heads].sum()) / (Hl * t)
+        ideal = {"attention": 1 / (1 - s_attn), "gemm_q": 1 / (1 - s_rows),
+                 "gemm_o_dispatch": 1 / (1 - s_rows)}
+        sp = {"gemm_q": dp[0] / parts[0], "attention": dp[1] / parts[1],
+              "gemm_o_dispatch": dp[2] / parts[2]}
+        line["dense_ms"] = {"gemm_q": round(dp[0], 4), "attention": round(dp[1], 4),
+                            "gemm_o_dispatch": round(dp[2], 4), "step": round(res["dense_ms"], 4)}
+        line["speedup_vs_dense"] = {k2: round(v2, 3) for k2, v2 in sp.items()}
+        line["speedup_vs_dense"]["step"] = round(res["dense_ms"] / ms, 3)
+        line["ideal_speedup"] = {k2: round(v2, 3) for k2, v2 in ideal.items()}
+        line["frac_sparsity_scaled_roofline"] = {k2: round(sp[k2] / ideal[k2], 3) for k2 in sp}
+        n_int = args.interval
+        line["gemm_o_amortized_ideal"] = round(n_int / (1 + (n_int - 1) * (1 - s_rows)), 3)
+        dense_attn_tflops = 4.0 * T * T * T * Hl * t * t / (dp[1] * 1e-3) / 1e12
+        line["dense_attention_tflops"] = round(dense_attn_tflops, 1)
+    if clocks is not None:
+        line["clocks"] = clocks.summary()
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        cms, sample, cparts = cpu_sample(cfg, cache_bits, skip_bits, args.seed)
+        line["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "cores": cpu_threads(),
+                                "kind": "port", "sample": sample,
+                                "breakdown_ms": {k2: round(v2, 1) for k2, v2 in cparts.items()}}
+    print(json.dumps(line), flush=True)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_b200(args, cfg, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

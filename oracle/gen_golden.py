@@ -1,0 +1,167 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation.
+
+    PYTHONPATH=/root/reference/pkg/src python oracle/gen_golden.py
+
+Imports `omniattn` from the read-only reference tree (numpy backend) in this
+container only; the fixtures are committed so nothing at test time needs
+/root/reference. Float inputs are rounded to bf16-representable values first,
+so the GPU engine (bf16 operands) and the reference (fp32) see identical
+numbers and the only difference left is arithmetic precision.
+"""
+
+import pathlib
+import sys
+
+import numpy as np
+
+REF = pathlib.Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+
+from omniattn import attention as ref_attn  # noqa: E402
+from omniattn import gemm as ref_gemm  # noqa: E402
+from omniattn import symbols as ref_sym  # noqa: E402
+from omniattn import verify as ref_verify  # noqa: E402
+
+OUT = pathlib.Path(__file__).resolve().parents[1] / "tests" / "golden"
+T = 128
+
+
+def bf16_bits(a):
+    """fp32 -> bf16 bit pattern (round to nearest even)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return r
+
+
+def from_bf16_bits(b):
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def bf16_round(a):
+    return from_bf16_bits(bf16_bits(a))
+
+
+def codec():
+    d = {}
+    idx = 0
+    for pool_n in (1, 2, 4):
+        rng = np.random.default_rng(100 + pool_n)
+        for _ in range(12):
+            t_q = int(rng.integers(1, 70))
+            t_kv = int(rng.integers(1, 70))
+            cb, sb = ref_verify.random_masks(rng, t_q, t_kv, pool_n)
+            sym = ref_sym.build_symbols(cb, sb, pool_n)
+            d[f"c{idx}_cache"] = cb
+            d[f"c{idx}_skip"] = sb
+            d[f"c{idx}_pool"] = np.array(pool_n)
+            d[f"c{idx}_sc"] = np.frombuffer(sym.s_c, np.uint8)
+            d[f"c{idx}_ss"] = np.frombuffer(sym.s_s, np.uint8)
+            d[f"c{idx}_blob"] = np.frombuffer(sym.to_bytes(), np.uint8)
+            idx += 1
+    d["n_cases"] = np.array(idx)
+    np.savez_compressed(OUT / "codec.npz", **d)
+
+
+def attention():
+    d = {}
+    cases = [(256, 1, 11), (300, 1, 12), (640, 2, 13)]
+    for ci, (n, pool_n, seed) in enumerate(cases):
+        rng = np.random.default_rng(seed)
+        t = -(-n // T)
+        q, k, v = (bf16_round(rng.standard_normal((n, T)).astype(np.float32)) for _ in range(3))
+        cb, sb = ref_verify.random_masks(rng, t, t, pool_n, density=0.5, cache_density=0.75)
+        sym = ref_sym.build_symbols(cb, sb, pool_n)
+        cache = ref_attn.FeatureCache(1, t, 0)
+        for i in range(t):
+            cache.update(0, i, v[i * T:min((i + 1) * T, n)])
+        ac = ref_attn.AttnCounters()
+        out = ref_attn.sparse_attention(q, k, v, sym, cache, 0, 1, 2, 0, b_q=T, b_k=T, mode="bias",
+                                        fill=np.nan, counters=ac)
+        p = f"a{ci}_"
+        d.update({p + "q": bf16_bits(q), p + "k": bf16_bits(k), p + "v": bf16_bits(v),
+                  p + "cache": cb, p + "skip": sb, p + "pool": np.array(pool_n),
+                  p + "out": out, p + "pairs": np.array(ac.pairs_computed),
+                  p + "total": np.array(ac.pairs_total)})
+    d["n_cases"] = np.array(len(cases))
+    np.savez_compressed(OUT / "attention.npz", **d)
+
+
+def gemm_q():
+    rng = np.random.default_rng(21)
+    n, dm, heads = 256, 256, 3
+    t = n // T
+    x = bf16_round(rng.standard_normal((n, dm)).astype(np.float32))
+    w_q = bf16_round((rng.standard_normal((heads, dm, T)) * dm ** -0.5).astype(np.float32))
+    norm = (1.0 + 0.05 * rng.standard_normal((heads, T))).astype(np.float32)
+    active = rng.random((t, heads)) < 0.6
+    active[0] = True
+    syms = [ref_sym.build_symbols(active[:, h], np.ones((t, t), bool), 1) for h in range(heads)]
+    gc = ref_gemm.GemmCounters()
+    disp = ref_gemm.project_q(x, w_q, norm, syms, "dispatch", b_q=T, counters=gc, fill=np.nan)
+    upd = ref_gemm.project_q(x, w_q, norm, None, "update", b_q=T)
+    np.savez_compressed(OUT / "gemm_q.npz", x=bf16_bits(x), w_q=bf16_bits(w_q), norm=norm,
+                        active=active, dispatch=disp, update=upd,
+                        q_macs_actual=np.array(gc.q_macs_actual),
+                        q_macs_dense=np.array(gc.q_macs_dense))
+
+
+def gemm_o():
+    rng = np.random.default_rng(31)
+    n, dm, heads, order, interval, elapsed = 256, 256, 3, 1, 5, 2
+    t = n // T
+    w_out = bf16_round((rng.standard_normal((heads, T, dm)) * T ** -0.5).astype(np.float32))
+    cache = ref_attn.FeatureCache(heads, t, order)
+    hist = []
+    for _ in range(order + 1):
+        o = bf16_round(rng.standard_normal((heads, n, T)).astype(np.float32))
+        hist.append(o)
+        for h in range(heads):
+            for i in range(t):
+                cache.update(h, i, o[h, i * T:(i + 1) * T])
+    o_cur = hist[-1]
+    active = rng.random((t, heads)) < 0.5
+    syms = [ref_sym.build_symbols(active[:, h], np.ones((t, t), bool), 1) for h in range(heads)]
+    out_u, bias = ref_gemm.project_out_update(o_cur, w_out, syms, cache, order, b_q=T)
+    o_disp = bf16_round(rng.standard_normal((heads, n, T)).astype(np.float32))
+    gc = ref_gemm.GemmCounters()
+    out_d = ref_gemm.project_out_dispatch(o_disp, w_out, syms, bias, elapsed, interval, order, b_q=T,
+                                          counters=gc)
+    bias_full = np.zeros((order + 1, n, dm), np.float32)
+    for i in range(t):
+        st = bias.stacks[i]
+        bias_full[:st.shape[0], i * T:(i + 1) * T] = st
+    np.savez_compressed(OUT / "gemm_o.npz", hist=np.stack([bf16_bits(a) for a in hist]),
+                        w_out=bf16_bits(w_out), active=active, out_update=out_u,
+                        bias=bias_full, orders=bias.orders, o_disp=bf16_bits(o_disp),
+                        out_dispatch=out_d, order=np.array(order),
+                        interval=np.array(interval), elapsed=np.array(elapsed),
+                        o_macs_actual=np.array(gc.o_macs_actual))
+
+
+def cache_push():
+    rng = np.random.default_rng(41)
+    rows, order = 128, 2
+    a, b, c = (bf16_round(rng.standard_normal((rows, T)).astype(np.float32)) for _ in range(3))
+    tiles, stacks, valids = [], [], []
+    e = None
+    for t_ in range(4):
+        tile = bf16_round((a + t_ * b + 0.25 * t_ * t_ * c).astype(np.float32))
+        e = ref_attn.update_entry(e, tile, order)
+        tiles.append(tile)
+        stacks.append(e.diff_stack.copy())
+        valids.append(e.valid_orders)
+    coef = ref_attn.forecast_coefficients(2, 4, order + 1)
+    fc = ref_attn.forecast(e, 2, 4, order)
+    np.savez_compressed(OUT / "cache.npz", tiles=np.stack([bf16_bits(x) for x in tiles]),
+                        stacks=np.stack(stacks), valids=np.array(valids), coef=coef, forecast=fc)
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    codec()
+    attention()
+    gemm_q()
+    gemm_o()
+    cache_push()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

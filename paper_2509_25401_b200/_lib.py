@@ -53,6 +53,20 @@ ST_CONSISTENCY, ST_STATE, ST_BOUNDS, ST_PARAM, ST_TIMEOUT = 0x1, 0x2, 0x4, 0x8, 
 
 _lib = None
 
+# entry points that launch exactly one kernel (gpu_launches accounting)
+LAUNCHING = {"fo_encode_symbols", "fo_decode_symbols", "fo_plan", "fo_sparse_attention",
+             "fo_forecast_materialize", "fo_cache_push", "fo_gemm_q", "fo_gemm_o_update",
+             "fo_gemm_o_dispatch", "fo_check_active_match"}
+_launches = [0]
+
+
+def reset_launch_count():
+    _launches[0] = 0
+
+
+def launch_count():
+    return _launches[0]
+
 
 def load():
     """Load the extension (once). Raises DeviceError when it is absent."""
@@ -81,6 +95,8 @@ def call(name, *args):
     reference exception class."""
     lib = load()
     rc = getattr(lib, name)(*args)
+    if name in LAUNCHING and rc == 0:
+        _launches[0] += 1
     if rc:
         msg = lib.fo_last_error().decode(errors="replace")
         raise _CODE_ERRORS.get(rc, DeviceError)(f"{name}: {msg}")
