@@ -231,16 +231,27 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         reg_fence(u[2]);
         reg_fence(u[3]);
         const bool mask_tail = tail && (j == n - 1);
-        float mx = -INFINITY;
+        float sv[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            float v = __uint_as_float(u[c][k]);
-            if (mask_tail && (c * 32 + k) >= last_valid) v = -INFINITY;
-            u[c][k] = __float_as_uint(v);
-            mx = fmaxf(mx, v);
-          }
+          for (int k = 0; k < 32; ++k) sv[c * 32 + k] = __uint_as_float(u[c][k]);
+        if (mask_tail) {
+          // key columns past the sequence end in the last (partial) block
+#pragma unroll
+          for (int k = 0; k < 128; ++k)
+            if (k >= last_valid) sv[k] = -INFINITY;
+        }
+        // row max: four independent FMNMX3 chains
+        float mc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float a = fmax3f(sv[32 * c], sv[32 * c + 1], sv[32 * c + 2]);
+#pragma unroll
+          for (int k = 3; k < 31; k += 2) a = fmax3f(a, sv[32 * c + k], sv[32 * c + k + 1]);
+          mc[c] = fmaxf(a, sv[32 * c + 31]);
+        }
+        const float mx = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
         const float m_tile = mx * p.scale_log2;
         bool need = false;
         float m_new;
@@ -254,19 +265,40 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         }
         const float corr = need ? fast_exp2(m_run - m_new) : 1.f;
         m_run = m_new;
-        float sum0 = 0.f, sum1 = 0.f;
+        // P = 2^(s*scale - m): packed FFMA2, exp2 split between the MUFU (5/8
+        // of the pairs) and an FMA-pipe polynomial (3/8), packed FADD2 row sums
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2 = make_float2(-m_new, -m_new);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
         uint32_t pk[2][32];
+        if (!mask_tail) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float p0 = fast_exp2(fmaf(__uint_as_float(u[c][2 * k]), p.scale_log2, -m_new));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(u[c][2 * k + 1]), p.scale_log2, -m_new));
-            sum0 += p0;
-            sum1 += p1;
-            pk[c >> 1][(c & 1) * 16 + k] = pack_bf16x2(p0, p1);
+          for (int q = 0; q < 64; ++q) {
+            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
+            float2 e;
+            if ((q & 7) < 3) {
+              e = exp2_poly2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
+            }
+            acc[q & 3] = fadd2(acc[q & 3], e);
+            pk[q >> 5][q & 31] = pack_bf16x2(e.x, e.y);
           }
-        l = l * corr + (sum0 + sum1);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 64; ++q) {
+            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
+            float2 e;
+            e.x = fast_exp2(x.x);  // exact zeros for the masked (-inf) columns
+            e.y = fast_exp2(x.y);
+            acc[q & 3] = fadd2(acc[q & 3], e);
+            pk[q >> 5][q & 31] = pack_bf16x2(e.x, e.y);
+          }
+        }
+        const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        l = l * corr + (s01.x + s01.y);
         tmem_st32(sa + 0, pk[0]);
         tmem_st32(sa + 32, pk[1]);
         tmem_st_wait();

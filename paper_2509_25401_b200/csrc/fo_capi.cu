@@ -143,7 +143,8 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
   if (rc) return rc;
   if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
   PlanView pv = plan_view(plan_ws, heads, rows);
-  const size_t smem = (size_t)(2 * (cols + 2) + 1024) * sizeof(int);
+  const bool head_major = (size_t)(heads * (cols + 2) + 1024) * sizeof(int) <= 160 * 1024;
+  const size_t smem = (size_t)((head_major ? heads : 1) * (cols + 2) + 1024) * sizeof(int);
   if (smem > 200 * 1024) return fail(FO_ERR_PARAM, "too many key blocks (%d)", cols);
   static bool configured = false;
   if (!configured) {

@@ -214,14 +214,29 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float o[32];
+          // 16-byte vector loads of the norm weights and the rotary table
+          float wv[32], cvv[16], svv[16];
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 t4 = __ldg(reinterpret_cast<const float4*>(nw + c * 32) + q4);
+            wv[4 * q4] = t4.x; wv[4 * q4 + 1] = t4.y; wv[4 * q4 + 2] = t4.z; wv[4 * q4 + 3] = t4.w;
+          }
+          if (rope) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const float4 a4 = __ldg(reinterpret_cast<const float4*>(cs + c * 16) + q4);
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(sn + c * 16) + q4);
+              cvv[4 * q4] = a4.x; cvv[4 * q4 + 1] = a4.y; cvv[4 * q4 + 2] = a4.z; cvv[4 * q4 + 3] = a4.w;
+              svv[4 * q4] = b4.x; svv[4 * q4 + 1] = b4.y; svv[4 * q4 + 2] = b4.z; svv[4 * q4 + 3] = b4.w;
+            }
+          }
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             // interleaved-pair RoPE (tensor.py:83-109)
-            const int col = c * 32 + 2 * k;
-            const float e = __uint_as_float(u[c][2 * k]) * __ldg(nw + col) * inv;
-            const float od = __uint_as_float(u[c][2 * k + 1]) * __ldg(nw + col + 1) * inv;
+            const float e = __uint_as_float(u[c][2 * k]) * wv[2 * k] * inv;
+            const float od = __uint_as_float(u[c][2 * k + 1]) * wv[2 * k + 1] * inv;
             if (rope) {
-              const float cv = __ldg(cs + col / 2), sv = __ldg(sn + col / 2);
+              const float cv = cvv[k], sv = svv[k];
               o[2 * k] = e * cv - od * sv;
               o[2 * k + 1] = e * sv + od * cv;
             } else {

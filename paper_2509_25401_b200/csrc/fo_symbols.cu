@@ -122,17 +122,21 @@ __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
             PlanView pv, uint32_t* status) {
+  // Attention items are ordered head-major, longest rows first within a head:
+  // CTAs stride through the list together, so the K/V of the ~1-2 heads in
+  // flight stay L2-resident while per-CTA work stays balanced.
   extern __shared__ int plan_smem[];
-  int* hist = plan_smem;        // [cols + 2]
-  int* offs = hist + cols + 2;  // [cols + 2]
-  int* scan = offs + cols + 2;  // [1024]
+  const int nseg = (H * (cols + 2) + 1024) * (int)sizeof(int) <= 160 * 1024 ? H : 1;
+  int* hist = plan_smem;                   // [nseg][cols + 2] -> exclusive offsets
+  int* scan = hist + nseg * (cols + 2);    // [1024]
   __shared__ unsigned long long s_pairs[64];
   const int comp_rows = ceil_div_d(rows, pool_n), comp_cols = ceil_div_d(cols, pool_n);
   const int sc_len = ceil_div_d(comp_rows, 8), row_stride = ceil_div_d(comp_cols, 8);
   const int tid = threadIdx.x, nt = blockDim.x;
   const int total = H * rows;
+  auto seg = [&](int h) { return nseg == 1 ? 0 : h; };
 
-  for (int c = tid; c < cols + 2; c += nt) hist[c] = 0;
+  for (int c = tid; c < nseg * (cols + 2); c += nt) hist[c] = 0;
   for (int h = tid; h < 64; h += nt) s_pairs[h] = 0;
   __syncthreads();
 
@@ -176,7 +180,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
         // active query block with every key block skipped (pyref.py:43-46)
         raise_status(status, ST_CONSISTENCY);
       } else {
-        atomicAdd(&hist[cnt], 1);
+        atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
         atomicAdd(&s_pairs[h], (unsigned long long)cnt);
       }
     } else if (valid && valid[(size_t)h * rows + i] < 1) {
@@ -185,13 +189,15 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     }
   }
   __syncthreads();
-  // descending exclusive scan of the histogram (longest rows first)
+  // exclusive scan: segment-major, descending KV count within a segment
   if (tid == 0) {
     int run = 0;
-    for (int c = cols; c >= 1; --c) {
-      offs[c] = run;
-      run += hist[c];
-    }
+    for (int g = 0; g < nseg; ++g)
+      for (int c = cols; c >= 1; --c) {
+        const int n = hist[g * (cols + 2) + c];
+        hist[g * (cols + 2) + c] = run;
+        run += n;
+      }
     pv.counts[0] = run;  // attention items
   }
   for (int h = tid; h < H; h += nt) pv.pairs_pred[h] = (long long)s_pairs[h];
@@ -202,7 +208,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     if (is_active(h, i)) {
       int cnt = kv_count(h, i);
       if (cnt > 0) {
-        int pos = atomicAdd(&offs[cnt], 1);
+        int pos = atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
         pv.items[pos] = make_int2((h << 20) | i, cnt);
       }
     }
