@@ -22,6 +22,23 @@
 // TMEM: O cols [0,128), S0 [128,256), S1 [256,384).
 #include "fo_internal.cuh"
 
+// pairs (out of every 8) whose exp2 runs as an FMA-pipe polynomial instead of
+// on the MUFU
+#ifndef FO_POLY_OF_8
+#define FO_POLY_OF_8 3
+#endif
+
+#ifdef FO_ATTN_TIMING
+#define TSTAMP(k)                     \
+  if (tim) {                          \
+    const long long _t = clock64();   \
+    tacc[k] += _t - tlast;            \
+    tlast = _t;                       \
+  }
+#else
+#define TSTAMP(k)
+#endif
+
 namespace fo {
 namespace attn {
 constexpr int KST = 3, VST = 2;
@@ -98,96 +115,127 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF;
-      if (lane == 0) {
-        mbar_wait(&bars->q_empty, (qi & 1) ^ 1, p.status);
+      mbar_wait(&bars->q_empty, (qi & 1) ^ 1, p.status);
+      if (elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
         tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, i * kTile);
         tma_load_2d(sQ + HALF_BYTES, &qm, &bars->q_full, h * kTile + 64, i * kTile);
       }
+      __syncwarp();
       const uint8_t* sym = p.s_s + h * head_sym;
       for (int base = 0; base < p.t_kv; base += 32) {
         const int j = base + lane;
         const uint32_t bit =
             (j < p.t_kv) && (p.dense || decode_reduction(sym, p.row_stride, i, j, p.pool_n));
-        uint32_t m = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) {
-          while (m) {
-            const int jj = base + __ffs(m) - 1;
-            m &= m - 1;
-            mbar_wait(&bars->k_empty[kst], kph ^ 1, p.status);
+        uint32_t m = __ballot_sync(0xffffffffu, bit);  // warp-uniform
+        while (m) {
+          const int jj = base + __ffs(m) - 1;
+          m &= m - 1;
+          mbar_wait(&bars->k_empty[kst], kph ^ 1, p.status);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&bars->k_full[kst], TILE_BYTES);
             uint8_t* dk = sK + kst * TILE_BYTES;
             tma_load_2d(dk, &km, &bars->k_full[kst], h * kTile, jj * kTile);
             tma_load_2d(dk + HALF_BYTES, &km, &bars->k_full[kst], h * kTile + 64, jj * kTile);
-            if (++kst == KST) {
-              kst = 0;
-              kph ^= 1;
-            }
-            mbar_wait(&bars->v_empty[vst], vph ^ 1, p.status);
+          }
+          __syncwarp();
+          if (++kst == KST) {
+            kst = 0;
+            kph ^= 1;
+          }
+          mbar_wait(&bars->v_empty[vst], vph ^ 1, p.status);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
             uint8_t* dv = sV + vst * TILE_BYTES;
             tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
             tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
-            if (++vst == VST) {
-              vst = 0;
-              vph ^= 1;
-            }
+          }
+          __syncwarp();
+          if (++vst == VST) {
+            vst = 0;
+            vph ^= 1;
           }
         }
-        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // The whole warp runs the schedule (every value stays warp-uniform, so the
+    // descriptors live in uniform registers); one elected lane issues the MMAs
+    // and the commits that track them.
+    {
       const uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
       const uint32_t idesc_pv = make_idesc_bf16(128, 128, false, true);
       int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
       uint32_t qk_cnt = 0, pv_cnt = 0;
-      const uint32_t qa = smem_u32(sQ);
+      // descriptor of K-chunk k (16 elements) of a K-major SW128 tile: +32 B within a
+      // 64-column half, +16 KB to the second half (start address is in 16 B units)
+      const uint64_t qdesc = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t kdesc0 = make_sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t vdesc0 = make_sdesc_sw128(smem_u32(sV), HALF_BYTES, 1024);
+#ifdef FO_ATTN_TIMING
+      const bool tim = p.dbg != nullptr && lane == 0;
+      long long tacc[16] = {0};
+      long long tlast = clock64();
+#endif
       auto issue_qk = [&]() {
+        TSTAMP(11);
         mbar_wait(&bars->k_full[kst], kph, p.status);
+        TSTAMP(10);
         tc_fence_after();
         const uint32_t sb = qk_cnt & 1;
         const uint32_t d = tbase + TM_S0 + sb * 128;
-        const uint32_t ka = smem_u32(sK + kst * TILE_BYTES);
+        const uint64_t kdesc = kdesc0 + (uint64_t)((kst * TILE_BYTES) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t off = (k >> 2) * HALF_BYTES + (k & 3) * 32;
-          mma_bf16_ss(d, make_sdesc_sw128(qa + off, 16, 1024), make_sdesc_sw128(ka + off, 16, 1024),
-                      idesc_qk, k > 0);
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t off = (uint64_t)((k >> 2) * (HALF_BYTES >> 4) + (k & 3) * 2);
+            mma_bf16_ss(d, qdesc + off, kdesc + off, idesc_qk, k > 0);
+          }
+          tc_commit(&bars->k_empty[kst]);
+          tc_commit(&bars->s_full[sb]);
         }
-        tc_commit(&bars->k_empty[kst]);
-        tc_commit(&bars->s_full[sb]);
+        __syncwarp();
         if (++kst == KST) {
           kst = 0;
           kph ^= 1;
         }
         ++qk_cnt;
       };
+      auto commit_q_empty = [&]() {
+        if (elect_one()) tc_commit(&bars->q_empty);
+        __syncwarp();
+      };
       for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
         const int n = p.items[w].y;
         mbar_wait(&bars->q_full, qi & 1, p.status);
         tc_fence_after();
         issue_qk();
-        if (n == 1) tc_commit(&bars->q_empty);
+        if (n == 1) commit_q_empty();
         for (int j = 0; j < n; ++j) {
           if (j + 1 < n) {
             issue_qk();
-            if (j + 2 == n) tc_commit(&bars->q_empty);
+            if (j + 2 == n) commit_q_empty();
           }
+          TSTAMP(8);
           mbar_wait(&bars->p_full, pv_cnt & 1, p.status);
+          TSTAMP(9);
           if (j == 0 && qi > 0) mbar_wait(&bars->o_free, (qi - 1) & 1, p.status);
+          TSTAMP(12);
           mbar_wait(&bars->v_full[vst], vph, p.status);
+          TSTAMP(13);
           tc_fence_after();
           const uint32_t a_t = tbase + TM_S0 + (pv_cnt & 1) * 128;
-          const uint32_t va = smem_u32(sV + vst * TILE_BYTES);
+          const uint64_t vdesc = vdesc0 + (uint64_t)((vst * TILE_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            mma_bf16_ts(tbase + TM_O, a_t + k * 8, make_sdesc_sw128(va + k * 2048, HALF_BYTES, 1024),
-                        idesc_pv, (j > 0 || k > 0));
-          tc_commit(&bars->v_empty[vst]);
-          tc_commit(&bars->o_done);
+            for (int k = 0; k < 8; ++k)
+              mma_bf16_ts(tbase + TM_O, a_t + k * 8, vdesc + (uint64_t)(k * (2048 >> 4)), idesc_pv,
+                          (j > 0 || k > 0));
+            tc_commit(&bars->v_empty[vst]);
+            tc_commit(&bars->o_done);
+          }
+          __syncwarp();
           if (++vst == VST) {
             vst = 0;
             vph ^= 1;
@@ -195,6 +243,10 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
           ++pv_cnt;
         }
       }
+#ifdef FO_ATTN_TIMING
+      if (tim)
+        for (int q = 8; q < 16; ++q) p.dbg[blockIdx.x * 32 + 16 + q] = tacc[q];
+#endif
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -206,6 +258,11 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     const size_t HD = (size_t)p.H * kTile;
     const size_t stack_stride = (size_t)p.S * HD;
     uint32_t qk_seen = 0, o_seen = 0;
+#ifdef FO_ATTN_TIMING
+    const bool tim = (r == 0) && p.dbg;
+    long long tacc[16] = {0};
+    long long tlast = clock64();
+#endif
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF, n = it.y;
@@ -216,7 +273,9 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
       float m_run = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         const uint32_t sb = qk_seen & 1;
+        TSTAMP(7);
         mbar_wait(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
+        TSTAMP(0);
         tc_fence_after();
         ++qk_seen;
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
@@ -226,6 +285,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         tmem_ld32(sa + 64, u[2]);
         tmem_ld32(sa + 96, u[3]);
         tmem_ld_wait();
+        TSTAMP(1);
         reg_fence(u[0]);
         reg_fence(u[1]);
         reg_fence(u[2]);
@@ -253,6 +313,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         }
         const float mx = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
         const float m_tile = mx * p.scale_log2;
+        TSTAMP(2);
         bool need = false;
         float m_new;
         if (j == 0) {
@@ -277,7 +338,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
           for (int q = 0; q < 64; ++q) {
             const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
             float2 e;
-            if ((q & 7) < 3) {
+            if ((q & 7) < FO_POLY_OF_8) {
               e = exp2_poly2(x);
             } else {
               e.x = fast_exp2(x.x);
@@ -300,8 +361,10 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
         l = l * corr + (s01.x + s01.y);
         tmem_st32(sa + 0, pk[0]);
+        TSTAMP(3);
         tmem_st32(sa + 32, pk[1]);
         tmem_st_wait();
+        TSTAMP(4);
         if (j > 0) {
           // PV_{j-1} must be complete before O can be rescaled for P_j
           mbar_wait(&bars->o_done, o_seen & 1, p.status);
@@ -322,8 +385,10 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
             tmem_st_wait();
           }
         }
+        TSTAMP(5);
         tc_fence_before();
         mbar_arrive(&bars->p_full);
+        TSTAMP(6);
       }
       // ---------------- epilogue: O / l -> bf16 -> HBM (+ feature-cache push)
       mbar_wait(&bars->o_done, o_seen & 1, p.status);
@@ -407,6 +472,10 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
       }
     }
+#ifdef FO_ATTN_TIMING
+    if (tim)
+      for (int q = 0; q < 16; ++q) p.dbg[blockIdx.x * 32 + q] = tacc[q];
+#endif
   }
   tc_fence_before();
   __syncthreads();

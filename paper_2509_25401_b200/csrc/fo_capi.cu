@@ -92,6 +92,15 @@ int check_head_dim(int head_dim) {
 }
 }  // namespace
 
+#ifdef FO_ATTN_TIMING
+static long long* fo_dbg_ptr = nullptr;
+extern "C" __attribute__((visibility("default"))) int fo_debug_timing(long long* host) {
+  if (!fo_dbg_ptr) return 1;
+  cudaMemcpy(host, fo_dbg_ptr, 148 * 32 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
+#endif
+
 extern "C" {
 
 int fo_abi_version(void) { return 1; }
@@ -171,6 +180,7 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
     return fail(FO_ERR_SHAPE, "symbols dimensioned %dx%d, expected %dx%d", rows, cols, t, t);
   if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3], got %d", order_d);
   if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  if (cols > 2048) return fail(FO_ERR_PARAM, "at most 2048 key blocks (262,144 tokens), got %d", cols);
   CUtensorMap qm, km, vm;
   const uint64_t HD = (uint64_t)heads * kTile;
   if ((rc = make_map(&qm, q, seq, HD, kTile, "q"))) return rc;
@@ -196,6 +206,16 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
   p.order_d = order_d;
   p.pairs = reinterpret_cast<long long*>(pairs);
   p.status = status;
+  p.dbg = nullptr;
+#ifdef FO_ATTN_TIMING
+  static long long* g_dbg = nullptr;
+  if (!g_dbg) {
+    cudaMalloc(&g_dbg, 148 * 32 * sizeof(long long));
+    cudaMemset(g_dbg, 0, 148 * 32 * sizeof(long long));
+  }
+  p.dbg = g_dbg;
+  fo_dbg_ptr = g_dbg;
+#endif
   if (!update_mode && !s_s) return fail(FO_ERR_PARAM, "s_s is NULL");
   launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
   return check_launch("sparse_attention");

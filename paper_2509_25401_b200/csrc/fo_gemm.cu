@@ -57,13 +57,13 @@ struct Ring {
   }
 };
 
-// issue one BK=64 k-block: 4 x (128x128x16) MMAs
-__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint32_t a_smem, uint32_t b_smem,
+// issue one BK=64 k-block: 4 x (128x128x16) MMAs from warp-uniform descriptors
+// (K-chunk k of a SW128 K-major tile starts 32 B = 2 descriptor units further)
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                            uint32_t idesc, bool acc_in) {
 #pragma unroll
   for (int k = 0; k < BK / 16; ++k)
-    mma_bf16_ss(d_tmem, make_sdesc_sw128(a_smem + k * 32, 16, 1024),
-                make_sdesc_sw128(b_smem + k * 32, 16, 1024), idesc, (acc_in || k > 0) ? 1u : 0u);
+    mma_bf16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (acc_in || k > 0) ? 1u : 0u);
 }
 
 template <int N>
@@ -122,44 +122,48 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
-      Ring rg;
-      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
-        int h, i;
-        job(w, h, i);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+    // TMA producer (whole warp walks the schedule; one elected lane issues)
+    Ring rg;
+    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+      int h, i;
+      job(w, h, i);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+        if (elect_one()) {
           uint8_t* st = smem + rg.s * STAGE_BYTES;
           mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
           tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
           tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h * BN);
-          rg.next();
         }
+        __syncwarp();
+        rg.next();
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
-      Ring rg;
-      int t = 0;
-      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
-        const int acc = t & 1;
-        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+    // MMA issuer (warp-uniform schedule, elected lane issues + commits)
+    const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+    const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
+    Ring rg;
+    int t = 0;
+    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+      const int acc = t & 1;
+      mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tbase + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&bars->full[rg.s], rg.ph);
         tc_fence_after();
-        const uint32_t d = tbase + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&bars->full[rg.s], rg.ph);
-          tc_fence_after();
-          const uint32_t a = smem_u32(smem + rg.s * STAGE_BYTES);
-          mma_kblock(d, a, a + A_BYTES, idesc, kb > 0);
+        const uint64_t a = desc0 + (uint64_t)((rg.s * STAGE_BYTES) >> 4);
+        if (elect_one()) {
+          mma_kblock(d, a, a + (A_BYTES >> 4), idesc, kb > 0);
           tc_commit(&bars->empty[rg.s]);
-          rg.next();
         }
-        tc_commit(&bars->tfull[acc]);
+        __syncwarp();
+        rg.next();
       }
+      if (elect_one()) tc_commit(&bars->tfull[acc]);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       Ring rg;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
         int i, nb, d;
@@ -318,10 +322,13 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
             m &= m - 1;
             for (int kk = 0; kk < 2; ++kk) {
               mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
-              uint8_t* st = smem + rg.s * STAGE_BYTES;
-              mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
-              tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
-              tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * BN);
+              if (elect_one()) {
+                uint8_t* st = smem + rg.s * STAGE_BYTES;
+                mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
+                tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
+                tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * BN);
+              }
+              __syncwarp();
               rg.next();
             }
           }
@@ -330,8 +337,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
       Ring rg;
       int t = 0;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
@@ -352,13 +360,17 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&bars->full[rg.s], rg.ph);
             tc_fence_after();
-            const uint32_t a = smem_u32(smem + rg.s * STAGE_BYTES);
-            mma_kblock(dst, a, a + A_BYTES, idesc, kb > 0);
-            tc_commit(&bars->empty[rg.s]);
+            const uint64_t a = desc0 + (uint64_t)((rg.s * STAGE_BYTES) >> 4);
+            if (elect_one()) {
+              mma_kblock(dst, a, a + (A_BYTES >> 4), idesc, kb > 0);
+              tc_commit(&bars->empty[rg.s]);
+            }
+            __syncwarp();
             rg.next();
           }
         }
-        tc_commit(&bars->tfull[acc]);
+        if (elect_one()) tc_commit(&bars->tfull[acc]);
+        __syncwarp();
         ++t;
       }
     }

@@ -71,6 +71,7 @@ struct AttnParams {
   int order_d;
   long long* pairs;       // [H] instrumented computed pairs, or null
   uint32_t* status;
+  long long* dbg;         // FO_ATTN_TIMING builds: per-CTA phase cycle counters
 };
 
 void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
