@@ -15,17 +15,18 @@
 //               (the "register run cache" of PAPER.md:248) and streams Q and the
 //               surviving K/V tiles into a 3-deep K ring / 2-deep V ring.
 //   warp 1      tcgen05.mma issuer: S_j = Q K_j^T (SS) into one of two TMEM S
-//               buffers, O += P_j V_j (TS, P read straight from TMEM).
+//               buffers, O += P_j V_j and L += P_j 1 (TS, P read straight from
+//               TMEM; L is the softmax row sum, computed on the tensor core).
 //   warps 4..7  softmax: one thread per query row; S from TMEM, lazy rescale
 //               (threshold 2^8) of the TMEM O accumulator, P written back as bf16
 //               over the S columns; epilogue O/l -> bf16 -> HBM (+ cache push).
-// TMEM: O cols [0,128), S0 [128,256), S1 [256,384).
+// TMEM: O cols [0,128), L [128,144), S0 [256,384), S1 [384,512).
 #include "fo_internal.cuh"
 
 // pairs (out of every 8) whose exp2 runs as an FMA-pipe polynomial instead of
 // on the MUFU
 #ifndef FO_POLY_OF_8
-#define FO_POLY_OF_8 3
+#define FO_POLY_OF_8 2
 #endif
 
 #ifdef FO_ATTN_TIMING
@@ -46,7 +47,8 @@ constexpr int TILE_BYTES = kTile * kTile * 2;  // 32 KB bf16 tile
 constexpr int HALF_BYTES = TILE_BYTES / 2;     // 128 rows x 64 cols, 128B-swizzled
 constexpr int SMEM_TILES = 1 + KST + VST;
 constexpr int NTHREADS = 256;
-constexpr uint32_t TM_O = 0, TM_S0 = 128;
+constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
+constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (the B operand of the row-sum MMA)
 
 struct Bars {
   uint64_t q_full, q_empty;
@@ -56,7 +58,7 @@ struct Bars {
   uint64_t p_full, o_done, o_free;
   uint32_t tmem_base;
 };
-constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + 1024 + (int)sizeof(Bars);
+constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
 }  // namespace attn
 
 // keep the compiler from hoisting uses of tcgen05.ld results above the wait
@@ -77,7 +79,11 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
   uint8_t* sQ = smem;
   uint8_t* sK = smem + TILE_BYTES;
   uint8_t* sV = smem + TILE_BYTES * (1 + KST);
-  Bars* bars = reinterpret_cast<Bars*>(smem + TILE_BYTES * SMEM_TILES);
+  uint8_t* sOnes = smem + TILE_BYTES * SMEM_TILES;  // 1024-aligned
+  Bars* bars = reinterpret_cast<Bars*>(sOnes + ONES_BYTES);
+  for (int e = threadIdx.x; e < ONES_BYTES / 4; e += blockDim.x)
+    reinterpret_cast<uint32_t*>(sOnes)[e] = 0x3F803F80u;  // bf16 1.0 pairs
+  fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -166,6 +172,8 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     {
       const uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
       const uint32_t idesc_pv = make_idesc_bf16(128, 128, false, true);
+      const uint32_t idesc_l = make_idesc_bf16(128, 16, false, false);
+      const uint64_t ones_desc = make_sdesc_sw128(smem_u32(sOnes), 16, 1024);
       int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
       uint32_t qk_cnt = 0, pv_cnt = 0;
       // descriptor of K-chunk k (16 elements) of a K-major SW128 tile: +32 B within a
@@ -232,6 +240,11 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
             for (int k = 0; k < 8; ++k)
               mma_bf16_ts(tbase + TM_O, a_t + k * 8, vdesc + (uint64_t)(k * (2048 >> 4)), idesc_pv,
                           (j > 0 || k > 0));
+            // row sums on the tensor core: L += P . 1 (every B element is 1.0, so one
+            // descriptor serves all K chunks); l is then exactly sum(bf16(P))
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              mma_bf16_ts(tbase + TM_L, a_t + k * 8, ones_desc, idesc_l, (j > 0 || k > 0));
             tc_commit(&bars->v_empty[vst]);
             tc_commit(&bars->o_done);
           }
@@ -270,7 +283,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
                         (p.dense || decode_reduction(p.s_s + h * head_sym, p.row_stride, i,
                                                      p.t_kv - 1, p.pool_n));
       const int valid_old = (p.cache && p.valid) ? p.valid[(size_t)h * p.t_q + i] : 0;
-      float m_run = -INFINITY, l = 0.f;
+      float m_run = -INFINITY;
       for (int j = 0; j < n; ++j) {
         const uint32_t sb = qk_seen & 1;
         TSTAMP(7);
@@ -326,12 +339,12 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         }
         const float corr = need ? fast_exp2(m_run - m_new) : 1.f;
         m_run = m_new;
-        // P = 2^(s*scale - m): packed FFMA2, exp2 split between the MUFU (5/8
-        // of the pairs) and an FMA-pipe polynomial (3/8), packed FADD2 row sums
+        // P = 2^(s*scale - m): packed FFMA2; exp2 split between the MUFU and an
+        // FMA-pipe polynomial (FO_POLY_OF_8 of every 8 pairs), which balances the
+        // two pipes (packed fp32x2 ops cost 4 issue cycles per warp, MUFU 8)
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
         const float2 nm2 = make_float2(-m_new, -m_new);
-        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
+
         uint32_t pk[2][32];
         if (!mask_tail) {
 #pragma unroll
@@ -344,7 +357,6 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
               e.x = fast_exp2(x.x);
               e.y = fast_exp2(x.y);
             }
-            acc[q & 3] = fadd2(acc[q & 3], e);
             pk[q >> 5][q & 31] = pack_bf16x2(e.x, e.y);
           }
         } else {
@@ -354,12 +366,9 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
             float2 e;
             e.x = fast_exp2(x.x);  // exact zeros for the masked (-inf) columns
             e.y = fast_exp2(x.y);
-            acc[q & 3] = fadd2(acc[q & 3], e);
             pk[q >> 5][q & 31] = pack_bf16x2(e.x, e.y);
           }
         }
-        const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-        l = l * corr + (s01.x + s01.y);
         tmem_st32(sa + 0, pk[0]);
         TSTAMP(3);
         tmem_st32(sa + 32, pk[1]);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
           if (__any_sync(0xffffffffu, need)) {
             const uint32_t oa = tbase + lane_off + TM_O;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 5; ++c) {  // O and the row-sum columns
               uint32_t o[32];
               tmem_ld32(oa + c * 32, o);
               tmem_ld_wait();
@@ -394,7 +403,11 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
       mbar_wait(&bars->o_done, o_seen & 1, p.status);
       ++o_seen;
       tc_fence_after();
-      const float inv_l = 1.f / l;
+      uint32_t lsum[16];
+      tmem_ld16(tbase + lane_off + TM_L, lsum);
+      tmem_ld_wait();
+      reg_fence(lsum);
+      const float inv_l = 1.f / __uint_as_float(lsum[0]);
       const int row = i * kTile + r;
       const bool row_ok = row < p.S;
       const int vn = min(valid_old + 1, p.order_d + 1);
