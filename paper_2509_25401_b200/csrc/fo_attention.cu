@@ -55,7 +55,7 @@ struct Bars {
   uint64_t k_full[KST], k_empty[KST];
   uint64_t v_full[VST], v_empty[VST];
   uint64_t s_full[2];
-  uint64_t p_full, o_done, o_free;
+  uint64_t p_full, o_done, o_last, o_free;
   uint32_t tmem_base;
 };
 constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     mbar_init(&bars->s_full[1], 1);
     mbar_init(&bars->p_full, 128);
     mbar_init(&bars->o_done, 1);
+    mbar_init(&bars->o_last, 1);
     mbar_init(&bars->o_free, 128);
     fence_barrier_init();
     tma_prefetch_desc(&qm);
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
               mma_bf16_ts(tbase + TM_L, a_t + k * 8, ones_desc, idesc_l, (j > 0 || k > 0));
             tc_commit(&bars->v_empty[vst]);
             tc_commit(&bars->o_done);
+            if (j == n - 1) tc_commit(&bars->o_last);  // every PV of the item is done
           }
           __syncwarp();
           if (++vst == VST) {
@@ -270,13 +272,14 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     const int last_valid = p.S - (p.t_kv - 1) * kTile;  // valid key columns of the last block
     const size_t HD = (size_t)p.H * kTile;
     const size_t stack_stride = (size_t)p.S * HD;
-    uint32_t qk_seen = 0, o_seen = 0;
+    uint32_t qk_seen = 0, o_base = 0;  // o_base: PVs of all earlier items
 #ifdef FO_ATTN_TIMING
     const bool tim = (r == 0) && p.dbg;
     long long tacc[16] = {0};
     long long tlast = clock64();
 #endif
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    int qi = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF, n = it.y;
       const bool tail = (last_valid < kTile) &&
@@ -315,16 +318,17 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
           for (int k = 0; k < 128; ++k)
             if (k >= last_valid) sv[k] = -INFINITY;
         }
-        // row max: four independent FMNMX3 chains
-        float mc[4];
+        // row max: eight independent FMNMX3 chains of 16 values, then a 3-level tree
+        float mc[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float a = fmax3f(sv[32 * c], sv[32 * c + 1], sv[32 * c + 2]);
+        for (int c = 0; c < 8; ++c) {
+          float a = fmax3f(sv[16 * c], sv[16 * c + 1], sv[16 * c + 2]);
 #pragma unroll
-          for (int k = 3; k < 31; k += 2) a = fmax3f(a, sv[32 * c + k], sv[32 * c + k + 1]);
-          mc[c] = fmaxf(a, sv[32 * c + 31]);
+          for (int k = 3; k < 15; k += 2) a = fmax3f(a, sv[16 * c + k], sv[16 * c + k + 1]);
+          mc[c] = fmaxf(a, sv[16 * c + 15]);
         }
-        const float mx = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
+        const float mx = fmax3f(fmax3f(mc[0], mc[1], mc[2]), fmax3f(mc[3], mc[4], mc[5]),
+                                fmaxf(mc[6], mc[7]));
         const float m_tile = mx * p.scale_log2;
         TSTAMP(2);
         bool need = false;
@@ -374,12 +378,14 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         tmem_st32(sa + 32, pk[1]);
         tmem_st_wait();
         TSTAMP(4);
-        if (j > 0) {
-          // PV_{j-1} must be complete before O can be rescaled for P_j
-          mbar_wait(&bars->o_done, o_seen & 1, p.status);
-          ++o_seen;
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          // PV_{j-1} must be complete before O can be rescaled for P_j. Waits are
+          // taken only when a lane rescales: S_j's commit already tracked every
+          // PV before PV_{j-1}, so o_done has completed o_base+j-1 or o_base+j
+          // phases and the parity of completion o_base+j is unambiguous.
+          mbar_wait(&bars->o_done, (o_base + j - 1) & 1, p.status);
           tc_fence_after();
-          if (__any_sync(0xffffffffu, need)) {
+          {
             const uint32_t oa = tbase + lane_off + TM_O;
 #pragma unroll
             for (int c = 0; c < 5; ++c) {  // O and the row-sum columns
@@ -400,8 +406,8 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
         TSTAMP(6);
       }
       // ---------------- epilogue: O / l -> bf16 -> HBM (+ feature-cache push)
-      mbar_wait(&bars->o_done, o_seen & 1, p.status);
-      ++o_seen;
+      mbar_wait(&bars->o_last, qi & 1, p.status);  // one phase per item
+      o_base += n;
       tc_fence_after();
       uint32_t lsum[16];
       tmem_ld16(tbase + lane_off + TM_L, lsum);
