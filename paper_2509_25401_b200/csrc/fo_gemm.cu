@@ -293,10 +293,13 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   const int nord = UPDATE ? p.order_d + 1 : 1;
   const int n_jobs = p.t_q * nbn * nord;
   const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
-  // job decode; returns false for update jobs with no work (d >= orders[i])
+  // job decode, order-major (all d = 0 tiles first): the static round-robin over
+  // CTAs then stays balanced when the d >= 1 jobs of blocks without cached heads
+  // are skipped. Returns false for update jobs with no work (d >= orders[i]).
   auto job = [&](int w, int& i, int& nb, int& d) -> bool {
-    d = w % nord;
-    const int rest = w / nord;
+    const int per = p.t_q * nbn;
+    d = w / per;
+    const int rest = w - d * per;
     nb = rest % nbn;
     i = rest / nbn;
     return !(UPDATE && d > 0 && d >= p.orders[i]);
@@ -390,14 +393,41 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       const bool hasA = (d == 0) && act != 0ull;
       const bool hasB = UPDATE && cached != 0ull;
       const int no = UPDATE ? 0 : min(p.order_d + 1, p.orders[i]);
-      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
-      tc_fence_after();
       const int row = i * BM + r;
       const bool row_ok = row < p.S;
       const size_t obase = (size_t)row * p.dm + (size_t)nb * BN;
+      // dispatch: this thread's bias row segment (orders 0..1, 128 columns) is
+      // fetched into registers before the accumulator wait, so the HBM latency
+      // overlaps the mainloop instead of stalling each 32-column chunk; the next
+      // tile's rows are pulled into L2 meanwhile
+      uint4 bv[2][16];
+      if (!UPDATE) {
+#pragma unroll
+        for (int dd = 0; dd < 2; ++dd)
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            bv[dd][q] = (row_ok && dd < no)
+                            ? __ldg(reinterpret_cast<const uint4*>(p.bias + dd * SD + obase) + q)
+                            : make_uint4(0u, 0u, 0u, 0u);
+        const int wn = w + gridDim.x;
+        if (wn < n_jobs) {
+          const int i2 = wn / nbn, nb2 = wn % nbn;
+          const int row2 = i2 * BM + r;
+          const int no2 = min(p.order_d + 1, p.orders[i2]);
+          if (row2 < p.S)
+            for (int dd = 0; dd < no2; ++dd) {
+              const __nv_bfloat16* a = p.bias + dd * SD + (size_t)row2 * p.dm + (size_t)nb2 * BN;
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 64));
+            }
+        }
+      }
+      const float c0 = p.coef[0], c1 = p.coef[1];
+      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
       const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
       const uint32_t tB = tA + (UPDATE ? BN : 0);
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t ua[32], ub[32];
         if (hasA) tmem_ld32(tA + c * 32, ua);
@@ -420,13 +450,27 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           }
           if (hasB && p.orders[i] > d) gemm::store_bf16x32(p.bias + d * SD + obase + c * 32, b);
         } else {
-          for (int dd = 0; dd < no; ++dd) {
+#pragma unroll
+          for (int dd = 0; dd < 2; ++dd) {
+            const float cf = dd == 0 ? c0 : c1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 b4 = bv[dd][c * 4 + q];
+              const uint32_t w4[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {  // zero-filled when dd >= no
+                o[q * 8 + 2 * e] = fmaf(cf, bf16lo(w4[e]), o[q * 8 + 2 * e]);
+                o[q * 8 + 2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[q * 8 + 2 * e + 1]);
+              }
+            }
+          }
+          for (int dd = 2; dd < no; ++dd) {  // orders 2..3 (rare): direct loads
             const uint4* bsrc = reinterpret_cast<const uint4*>(p.bias + dd * SD + obase + c * 32);
             const float cf = p.coef[dd];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint4 bv = __ldg(bsrc + q);
-              const uint32_t w4[4] = {bv.x, bv.y, bv.z, bv.w};
+              const uint4 b4 = __ldg(bsrc + q);
+              const uint32_t w4[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 o[q * 8 + 2 * e] = fmaf(cf, bf16lo(w4[e]), o[q * 8 + 2 * e]);
