@@ -49,6 +49,7 @@ from .gemm import (
     rope_tables,
 )
 from .pipeline import (
+    HostStepper,
     LayerParams,
     LayerState,
     dispatch_step,

@@ -122,3 +122,48 @@ def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check
 def new_layer_state(params, seq, order_d):
     t_q = ceil_div(seq, TILE)
     return LayerState(params=params, cache=FeatureCache(params.heads, t_q, order_d, seq=seq))
+
+
+class HostStepper:
+    """Dispatch steps on host-resident activations with the PCIe copies
+    overlapped across steps: step k+1's input copy (H2D stream) and step k-1's
+    output copy (D2H stream) run while step k computes. Every step still moves
+    its own x in and its own out back; device buffers are double-buffered and
+    ordered by CUDA events, so no step reads a buffer the next copy is filling.
+    """
+
+    def __init__(self, state, seq, d_model, device=None, group=None):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.state, self.group = state, group
+        H = state.params.heads
+        self.h2d, self.d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self.x = [torch.empty(seq, d_model, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.out = [torch.empty(seq, d_model, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.bufs = {n: torch.empty(seq, H, TILE, dtype=torch.bfloat16, device=dev)
+                     for n in ("q", "k", "v", "o")}
+        ev = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
+        self.x_ready, self.x_free, self.out_ready, self.out_free = ev(), ev(), ev(), ev()
+        self.k = 0
+
+    def step(self, x_host, out_host, elapsed_k, interval_n, order_d):
+        """Enqueue one step (asynchronous; out_host is valid after synchronize)."""
+        b = self.k & 1
+        comp = torch.cuda.current_stream()
+        if self.k >= 2:
+            self.h2d.wait_event(self.x_free[b])
+        with torch.cuda.stream(self.h2d):
+            self.x[b].copy_(x_host, non_blocking=True)
+            self.x_ready[b].record(self.h2d)
+        comp.wait_event(self.x_ready[b])
+        if self.k >= 2:
+            comp.wait_event(self.out_free[b])
+        bufs = dict(self.bufs, out=self.out[b])
+        dispatch_step(self.state, self.x[b], elapsed_k, interval_n, order_d, group=self.group,
+                      check=False, bufs=bufs)
+        self.x_free[b].record(comp)
+        self.out_ready[b].record(comp)
+        self.d2h.wait_event(self.out_ready[b])
+        with torch.cuda.stream(self.d2h):
+            out_host.copy_(self.out[b], non_blocking=True)
+            self.out_free[b].record(self.d2h)
+        self.k += 1
