@@ -134,6 +134,23 @@ FO_API int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bia
 FO_API int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
                           int pool_n, uint32_t* status, void* stream);
 
+/* Update-step mask policy, all heads at once (replaces policy.py:196-234
+ * generate_masks, called per head from pipeline.py:260-270). q, k: bf16
+ * [seq, heads, 128] (head_dim 128, b_q = b_k = 128). n_text: leading text
+ * tokens. tau_q / tau_kv / s_q in [0, 1] (ramp_threshold is applied by the
+ * caller, policy.py:181-187). guard != 0 protects text columns and the
+ * diagonal. Outputs, True = compute: cache_bits u8 [heads, t_q], skip_bits u8
+ * [heads, t_q, t_q]; feed them to fo_encode_symbols. Decisions match the
+ * reference's float32 / float64 numpy bit for bit (see fo_policy.cu).
+ * Errors: PARAM for thresholds outside [0, 1] or a text prefix that leaves no
+ * vision row (policy.py:33-37), SHAPE for more than 1024 compressed blocks
+ * per side. */
+FO_API size_t fo_policy_workspace_bytes(int seq, int heads, int pool_n);
+FO_API int fo_generate_masks(const void* q, const void* k, int seq, int heads, int n_text,
+                             int pool_n, double tau_q, double tau_kv, double s_q, int guard,
+                             uint8_t* cache_bits, uint8_t* skip_bits, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@ sys.path.insert(0, str(REF))
 from omniattn import attention as ref_attn  # noqa: E402
 from omniattn import gemm as ref_gemm  # noqa: E402
 from omniattn import symbols as ref_sym  # noqa: E402
+from omniattn import policy as ref_policy  # noqa: E402
 from omniattn import verify as ref_verify  # noqa: E402
 
 OUT = pathlib.Path(__file__).resolve().parents[1] / "tests" / "golden"
@@ -156,8 +157,38 @@ def cache_push():
                         stacks=np.stack(stacks), valids=np.array(valids), coef=coef, forecast=fc)
 
 
+def policy():
+    """generate_masks (policy.py:196-234) on structured bf16-representable q/k:
+    a text prefix plus vision tokens whose blocks share a random direction, so
+    the pooled map has real structure and the selections are non-trivial."""
+    d = {}
+    cases = [  # (n, n_text, pool_n, tau_q, tau_kv, s_q, guard, seed)
+        (1536, 256, 1, 0.3, 0.2, 0.0, True, 51),
+        (2048, 128, 1, 0.5, 0.4, 0.0, True, 52),
+        (1664, 300, 2, 0.4, 0.3, 0.0, True, 53),
+        (1024, 128, 1, 0.6, 0.5, 0.9, True, 54),
+        (1280, 200, 1, 0.2, 0.6, 0.0, False, 55),
+    ]
+    for ci, (n, n_text, pool, tq, tkv, sq, guard, seed) in enumerate(cases):
+        rng = np.random.default_rng(seed)
+        t = -(-n // T)
+        base_q = rng.standard_normal((t, T)) * 1.5
+        base_k = rng.standard_normal((t, T)) * 1.5
+        q = np.repeat(base_q, T, 0)[:n] + rng.standard_normal((n, T))
+        k = np.repeat(base_k, T, 0)[:n] + rng.standard_normal((n, T))
+        q, k = bf16_round(q.astype(np.float32)), bf16_round(k.astype(np.float32))
+        cb, sb = ref_policy.generate_masks(q, k, b_q=T, b_k=T, pool_n=pool, n_text=n_text,
+                                           tau_q=tq, tau_kv=tkv, s_q=sq, guard=guard)
+        p = f"p{ci}_"
+        d.update({p + "q": bf16_bits(q), p + "k": bf16_bits(k), p + "cache": cb, p + "skip": sb,
+                  p + "args": np.array([n, n_text, pool, tq, tkv, sq, float(guard)], np.float64)})
+    d["n_cases"] = np.array(len(cases))
+    np.savez_compressed(OUT / "policy.npz", **d)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
+    policy()
     codec()
     attention()
     gemm_q()

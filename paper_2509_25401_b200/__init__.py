@@ -58,6 +58,7 @@ from .pipeline import (
     shard_heads,
     update_step,
 )
+from .policy import MaskPolicy, generate_masks, generate_masks_heads, ramp_threshold
 from ._kernels import available_backends, get_backend
 
 __version__ = "0.1.0"

@@ -22,6 +22,7 @@ LIB_PATH = pathlib.Path(__file__).with_name("_fo_b200.so")
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _F = ctypes.c_float
+_D = ctypes.c_double
 _SZ = ctypes.c_size_t
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -42,9 +43,11 @@ SIGNATURES = {
     "fo_gemm_o_update": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "fo_gemm_o_dispatch": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
     "fo_check_active_match": [_P, _P, _I, _I, _I, _P, _P],
+    "fo_policy_workspace_bytes": [_I, _I, _I],
+    "fo_generate_masks": [_P, _P, _I, _I, _I, _I, _D, _D, _D, _I, _P, _P, _P, _SZ, _P],
 }
 _RESTYPES = {"fo_last_error": ctypes.c_char_p, "fo_plan_workspace_bytes": _SZ,
-             "fo_plan_offsets": None}
+             "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ}
 
 # return codes / status bits (flashomni_b200.h)
 _CODE_ERRORS = {1: ShapeError, 2: ParameterError, 3: BoundsError, 4: ConsistencyError,
@@ -53,10 +56,12 @@ ST_CONSISTENCY, ST_STATE, ST_BOUNDS, ST_PARAM, ST_TIMEOUT = 0x1, 0x2, 0x4, 0x8, 
 
 _lib = None
 
-# entry points that launch exactly one kernel (gpu_launches accounting)
-LAUNCHING = {"fo_encode_symbols", "fo_decode_symbols", "fo_plan", "fo_sparse_attention",
-             "fo_forecast_materialize", "fo_cache_push", "fo_gemm_q", "fo_gemm_o_update",
-             "fo_gemm_o_dispatch", "fo_check_active_match"}
+# entry point -> kernels it launches (gpu_launches accounting)
+LAUNCHING = {n: 1 for n in ("fo_encode_symbols", "fo_decode_symbols", "fo_plan",
+                            "fo_sparse_attention", "fo_forecast_materialize", "fo_cache_push",
+                            "fo_gemm_q", "fo_gemm_o_update", "fo_gemm_o_dispatch",
+                            "fo_check_active_match")}
+LAUNCHING["fo_generate_masks"] = 5  # pool q, pool k, scores, cache select, skip select
 _launches = [0]
 
 
@@ -96,7 +101,7 @@ def call(name, *args):
     lib = load()
     rc = getattr(lib, name)(*args)
     if name in LAUNCHING and rc == 0:
-        _launches[0] += 1
+        _launches[0] += LAUNCHING[name]
     if rc:
         msg = lib.fo_last_error().decode(errors="replace")
         raise _CODE_ERRORS.get(rc, DeviceError)(f"{name}: {msg}")

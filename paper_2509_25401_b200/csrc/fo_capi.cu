@@ -357,4 +357,43 @@ int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads,
   return check_launch("check_active_match");
 }
 
+size_t fo_policy_workspace_bytes(int seq, int heads, int pool_n) {
+  if (seq <= 0 || heads <= 0 || pool_n <= 0) return 0;
+  const int rows_c = (seq + pool_n * kTile - 1) / (pool_n * kTile);
+  return policy_workspace_bytes(heads, rows_c);
+}
+
+int fo_generate_masks(const void* q, const void* k, int seq, int heads, int n_text, int pool_n,
+                      double tau_q, double tau_kv, double s_q, int guard, uint8_t* cache_bits,
+                      uint8_t* skip_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!q || !k || !cache_bits || !skip_bits || !workspace)
+    return fail(FO_ERR_PARAM, "generate_masks: null pointer");
+  if (seq <= 0 || heads <= 0) return fail(FO_ERR_SHAPE, "generate_masks: seq=%d heads=%d", seq, heads);
+  if (pool_n <= 0) return fail(FO_ERR_PARAM, "pool_n must be >= 1, got %d", pool_n);
+  if (n_text < 0 || n_text > seq)
+    return fail(FO_ERR_PARAM, "n_text=%d outside [0, %d]", n_text, seq);
+  // policy.py:101-102, 136-137, 168-169 (NaN fails these too)
+  if (!(tau_q >= 0.0 && tau_q <= 1.0)) return fail(FO_ERR_PARAM, "tau_q must be in [0, 1], got %g", tau_q);
+  if (!(tau_kv >= 0.0 && tau_kv <= 1.0))
+    return fail(FO_ERR_PARAM, "tau_kv must be in [0, 1], got %g", tau_kv);
+  if (!(s_q >= 0.0 && s_q <= 1.0)) return fail(FO_ERR_PARAM, "s_q must be in [0, 1], got %g", s_q);
+  const int block = pool_n * kTile;
+  const int rows_c = (seq + block - 1) / block;
+  const int n_t = (n_text + block - 1) / block;
+  if (rows_c > kPolicyMaxBlocks)
+    return fail(FO_ERR_SHAPE, "generate_masks: %d compressed blocks exceed %d", rows_c,
+                kPolicyMaxBlocks);
+  if (n_t >= rows_c)  // CompressedAttnMap.__post_init__ (policy.py:33-37)
+    return fail(FO_ERR_PARAM, "n_t=%d must leave at least one vision row (map has %d rows)", n_t,
+                rows_c);
+  if (workspace_bytes < policy_workspace_bytes(heads, rows_c))
+    return fail(FO_ERR_PARAM, "generate_masks: workspace %zu B < %zu B", workspace_bytes,
+                policy_workspace_bytes(heads, rows_c));
+  cudaError_t e = launch_generate_masks(
+      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), seq, heads, n_t,
+      pool_n, tau_q, tau_kv, s_q, guard, cache_bits, skip_bits, workspace, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "generate_masks: %s", cudaGetErrorString(e));
+  return FO_OK;
+}
+
 }  // extern "C"

@@ -113,4 +113,12 @@ void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t
 void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,
                        int t_q, int order_d, const uint8_t* sel, cudaStream_t stream);
 
+// update-step mask policy (fo_policy.cu)
+constexpr int kPolicyMaxBlocks = 1024;  // compressed blocks per side
+size_t policy_workspace_bytes(int H, int rows_c);
+cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k, int S, int H,
+                                  int n_t, int pool_n, double tau_q, double tau_kv, double s_q,
+                                  int guard, uint8_t* cache_bits, uint8_t* skip_bits, void* ws,
+                                  cudaStream_t stream);
+
 }  // namespace fo

@@ -1,0 +1,311 @@
+// Update-step mask policy on the GPU (reference policy.py:44-234).
+//
+// Turns fresh q/k into the next window's cache and skip masks without a host
+// round trip. The reference computes in float32 / float64 numpy; to reproduce
+// its decisions bit for bit the kernels follow numpy's reduction orders:
+//   mean_pool_blocks   fp64 sequential block sums / lengths -> fp32 (tensor.py:112-126)
+//   scores             fp64 dot products / sqrt(d) -> fp32 (policy.py:44-55)
+//   row_softmax        fp64 exp, numpy pairwise row sum, / sum -> fp32 (tensor.py:42-47)
+//   contribution       fp32 sequential column sums over text rows (policy.py:58-65)
+//   guidance           row_softmax of the transposed vision x text block, fp32
+//                      sequential column sums (policy.py:68-77)
+//   prefix selection   stable ascending order (ties -> lower index), fp64
+//                      sequential cumsum, csum <= budget (* total) (policy.py:80-121)
+// Four small launches: pool (thread per (head, block, dim)), scores (warp per
+// (head, compressed row)), cache selection (CTA per head), skip selection
+// (warp per (head, compressed row)). The compressed map of a 33K-token layer
+// is 258 x 258 per head, so all of it is a few tens of microseconds.
+#include "fo_internal.cuh"
+
+namespace fo {
+
+namespace {
+
+constexpr int kPolWarps = 4;  // warps per CTA in the per-row kernels
+
+__global__ void pool_kernel(const __nv_bfloat16* __restrict__ x, int S, int H, int block, int rows_c,
+                            float* __restrict__ out) {  // [H, rows_c, 128]
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= H * rows_c * kTile) return;
+  const int d = idx % kTile, r = (idx / kTile) % rows_c, h = idx / (kTile * rows_c);
+  const int s0 = r * block, s1 = min(S, s0 + block);
+  double acc = 0.0;  // np.add.reduceat: sequential from the first element
+  for (int s = s0; s < s1; ++s)
+    acc += (double)__bfloat162float(x[(size_t)s * H * kTile + (size_t)h * kTile + d]);
+  out[idx] = (float)(acc / (double)(s1 - s0));
+}
+
+__device__ double pairwise_leaf(const double* p, int n) {
+  if (n < 8) {
+    double res = 0.;
+    for (int i = 0; i < n; ++i) res += p[i];
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = p[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] += p[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += p[i];
+  return res;
+}
+
+// numpy's pairwise_sum (umath loops_utils.h): blocks of <= 128 with eight
+// accumulators, larger runs split at n/2 rounded down to a multiple of 8.
+template <int DEPTH>
+__device__ double pairwise_sum(const double* a, int n) {
+  if (n <= 128) return pairwise_leaf(a, n);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum<DEPTH - 1>(a, n2) + pairwise_sum<DEPTH - 1>(a + n2, n - n2);
+}
+template <>
+__device__ double pairwise_sum<0>(const double* a, int n) {
+  return pairwise_leaf(a, n);  // unreachable for n <= kPolicyMaxBlocks
+}
+
+// row_softmax of one fp32 row (length n >= 1) into out (fp32); e: fp64 scratch
+__device__ void row_softmax_serial(const float* s, int n, double* e, float* out) {
+  float mx = s[0];
+  for (int i = 1; i < n; ++i) mx = fmaxf(mx, s[i]);
+  for (int i = 0; i < n; ++i) e[i] = exp((double)s[i] - (double)mx);
+  const double sum = pairwise_sum<5>(e, n);
+  for (int i = 0; i < n; ++i) out[i] = (float)(e[i] / sum);
+}
+
+// warp per (head, compressed row): p_tilde[h, r, :]
+__global__ void scores_kernel(const float* __restrict__ pq, const float* __restrict__ pk, int H,
+                              int rows_c, float* __restrict__ p_tilde) {
+  extern __shared__ double pol_smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kPolWarps + wib;
+  if (gw >= H * rows_c) return;
+  const int cols = rows_c;
+  const int h = gw / rows_c, r = gw % rows_c;
+  double* e = pol_smem + (size_t)wib * cols * 2;
+  float* s = reinterpret_cast<float*>(e + cols);
+  const float* qr = pq + ((size_t)h * rows_c + r) * kTile;
+  const double rs = sqrt((double)kTile);
+  for (int c = lane; c < cols; c += 32) {
+    const float* kc = pk + ((size_t)h * cols + c) * kTile;
+    double acc = 0.0;
+    for (int d = 0; d < kTile; ++d) acc += (double)qr[d] * (double)kc[d];
+    s[c] = (float)(acc / rs);
+  }
+  __syncwarp();
+  if (lane == 0) row_softmax_serial(s, cols, e, p_tilde + ((size_t)h * rows_c + r) * cols);
+}
+
+// Stable ascending budget prefix over v[0, n) (fp64 copies of fp32 values).
+// Ranks by (value, index) in parallel; one lane scans the fp64 cumsum in rank
+// order. Returns cut: elements with rank < cut are taken.
+template <bool CTA>
+__device__ int budget_prefix(const double* v, int n, double budget, bool relative, int* rank,
+                             double* sorted, int tid, int nt) {
+  for (int i = tid; i < n; i += nt) {
+    const double vi = v[i];
+    int rk = 0;
+    for (int j = 0; j < n; ++j) {
+      const double vj = v[j];
+      rk += (vj < vi) || (vj == vi && j < i);
+    }
+    rank[i] = rk;
+    sorted[rk] = vi;
+  }
+  if (CTA) __syncthreads(); else __syncwarp();
+  int cut = 0;
+  if (tid == 0) {
+    // the relative total is csum[-1] of the same sequential cumsum
+    double lim = budget;
+    if (relative) {
+      double t = 0.0;
+      for (int k = 0; k < n; ++k) t += sorted[k];
+      lim = budget * t;
+    }
+    double c = 0.0;
+    for (; cut < n; ++cut) {
+      c += sorted[cut];
+      if (!(c <= lim)) break;
+    }
+  }
+  if (CTA) {
+    __shared__ int s_cut;
+    if (tid == 0) s_cut = cut;
+    __syncthreads();
+    cut = s_cut;
+    __syncthreads();
+  } else {
+    cut = __shfl_sync(0xffffffffu, cut, 0);
+  }
+  return cut;
+}
+
+// CTA per head: contribution / guidance -> compressed compute bits + degrade.
+__global__ void __launch_bounds__(256)
+cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, double tau_q,
+                    double s_q, uint8_t* __restrict__ comp_cache,  // [H, rows_c]
+                    double* __restrict__ gscratch) {               // [H, 4 * rows_c] doubles
+  extern __shared__ double cs_smem[];
+  const int h = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int cols = rows_c, V = rows_c - n_t;
+  const float* P = p_tilde + (size_t)h * rows_c * cols;
+  double* contrib = cs_smem;                                   // [V]
+  double* guid = contrib + rows_c;                             // [V]
+  double* sorted = guid + rows_c;                              // [V]
+  int* rank = reinterpret_cast<int*>(sorted + rows_c);         // [V]
+  uint8_t* cut_c = reinterpret_cast<uint8_t*>(rank + rows_c);  // [V]
+  uint8_t* cc = cut_c + rows_c;                                // [rows_c]
+  // vision_to_text_contribution: p[:n_t, n_t:].sum(axis=0), fp32 row by row
+  for (int c = tid; c < V; c += nt) {
+    float a = 0.f;
+    for (int r = 0; r < n_t; ++r) {
+      const float x = P[(size_t)r * cols + n_t + c];
+      a = r ? a + x : x;
+    }
+    contrib[c] = (double)a;
+  }
+  // text_to_vision_guidance: text column j re-softmaxed over the vision rows,
+  // then fp32 sums over j (serial: n_t is a handful of compressed blocks)
+  if (tid == 0) {
+    if (n_t > 0) {
+      double* e = gscratch + (size_t)h * 4 * rows_c;
+      float* tmp = reinterpret_cast<float*>(e + rows_c);
+      float* beta = tmp + rows_c;
+      float* acc = reinterpret_cast<float*>(e + 2 * rows_c);
+      for (int j = 0; j < n_t; ++j) {
+        for (int c = 0; c < V; ++c) tmp[c] = P[(size_t)(n_t + c) * cols + j];
+        row_softmax_serial(tmp, V, e, beta);
+        for (int c = 0; c < V; ++c) acc[c] = j ? acc[c] + beta[c] : beta[c];
+      }
+      for (int c = 0; c < V; ++c) guid[c] = (double)acc[c];
+    } else {
+      for (int c = 0; c < V; ++c) guid[c] = 0.0;
+    }
+  }
+  __syncthreads();
+  // select_cached_blocks: both ascending prefixes within tau_q of their totals
+  int cut = budget_prefix<true>(contrib, V, tau_q, true, rank, sorted, tid, nt);
+  for (int i = tid; i < V; i += nt) cut_c[i] = rank[i] < cut;
+  __syncthreads();
+  cut = budget_prefix<true>(guid, V, tau_q, true, rank, sorted, tid, nt);
+  for (int r = tid; r < rows_c; r += nt)
+    cc[r] = (r < n_t) ? 1 : !(cut_c[r - n_t] && rank[r - n_t] < cut);
+  __syncthreads();
+  // degrade_to_full_cache: computed vision fraction below s_q -> cache all vision
+  __shared__ int n_comp;
+  if (tid == 0) {
+    int c = 0;
+    for (int r = n_t; r < rows_c; ++r) c += cc[r];
+    n_comp = c;
+  }
+  __syncthreads();
+  const bool degrade = V > 0 && (double)n_comp / (double)V < s_q;
+  for (int r = tid; r < rows_c; r += nt)
+    comp_cache[(size_t)h * rows_c + r] = (degrade && r >= n_t) ? 0 : cc[r];
+}
+
+// warp per (head, compressed row): select_skip_blocks for computed rows, then
+// expand_blocks into block-granularity bits (policy.py:124-159, 190-193).
+__global__ void skip_select_kernel(const float* __restrict__ p_tilde,
+                                   const uint8_t* __restrict__ comp_cache, int H, int rows_c,
+                                   int n_t, double tau_kv, int guard, int pool_n, int t_q,
+                                   uint8_t* __restrict__ cache_bits,
+                                   uint8_t* __restrict__ skip_bits) {
+  extern __shared__ double sk_smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kPolWarps + wib;
+  if (gw >= H * rows_c) return;
+  const int cols = rows_c, t_kv = t_q;
+  const int h = gw / rows_c, r = gw % rows_c;
+  double* v = sk_smem + (size_t)wib * cols * 3;  // candidate scores
+  double* sorted = v + cols;
+  int* rank = reinterpret_cast<int*>(sorted + cols);
+  uint8_t* keep = reinterpret_cast<uint8_t*>(rank + cols);
+  const bool active = comp_cache[(size_t)h * rows_c + r] != 0;
+  const float* P = p_tilde + ((size_t)h * rows_c + r) * cols;
+  // guarded: text columns and the diagonal are protected (square map: r < cols)
+  const bool any_prot = guard != 0;
+  auto prot = [&](int c) { return guard && (c < n_t || c == r); };
+  // candidate k -> column: the unprotected columns in increasing order
+  auto cand_col = [&](int k) {
+    if (!guard) return k;
+    int c = n_t + k;
+    if (r >= n_t && c >= r) ++c;
+    return c;
+  };
+  const int nc = guard ? cols - n_t - (r >= n_t ? 1 : 0) : cols;
+  for (int c = lane; c < cols; c += 32) keep[c] = active && prot(c);
+  if (active && nc > 0) {
+    for (int k = lane; k < nc; k += 32) v[k] = (double)P[cand_col(k)];
+    __syncwarp();
+    const int cut = budget_prefix<false>(v, nc, tau_kv, false, rank, sorted, lane, 32);
+    int spare = -1;
+    if (!any_prot && cut == nc) {  // all skipped: spare argmax (first occurrence)
+      if (lane == 0) {
+        spare = 0;
+        for (int k = 1; k < nc; ++k)
+          if (v[k] > v[spare]) spare = k;
+      }
+      spare = __shfl_sync(0xffffffffu, spare, 0);
+    }
+    for (int k = lane; k < nc; k += 32)
+      if (rank[k] >= cut || k == spare) keep[cand_col(k)] = 1;
+  }
+  __syncwarp();
+  for (int rr = r * pool_n; rr < min((r + 1) * pool_n, t_q); ++rr) {
+    uint8_t* out = skip_bits + ((size_t)h * t_q + rr) * t_kv;
+    for (int j = lane; j < t_kv; j += 32) out[j] = keep[j / pool_n];
+    if (lane == 0) cache_bits[(size_t)h * t_q + rr] = active;
+  }
+}
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+size_t policy_workspace_bytes(int H, int rows_c) {
+  // pooled q, k [H, rows_c, 128] fp32 | p_tilde [H, rows_c, rows_c] fp32 |
+  // compressed compute bits [H, rows_c] | guidance scratch [H, 4 rows_c] fp64
+  return 2 * al256((size_t)H * rows_c * kTile * 4) + al256((size_t)H * rows_c * rows_c * 4) +
+         al256((size_t)H * rows_c) + al256((size_t)H * 4 * rows_c * 8);
+}
+
+cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k, int S, int H,
+                                  int n_t, int pool_n, double tau_q, double tau_kv, double s_q,
+                                  int guard, uint8_t* cache_bits, uint8_t* skip_bits, void* ws,
+                                  cudaStream_t stream) {
+  const int block = pool_n * kTile;
+  const int rows_c = (S + block - 1) / block;
+  const int t_q = (S + kTile - 1) / kTile;
+  char* w = static_cast<char*>(ws);
+  float* pq = reinterpret_cast<float*>(w);
+  w += al256((size_t)H * rows_c * kTile * 4);
+  float* pk = reinterpret_cast<float*>(w);
+  w += al256((size_t)H * rows_c * kTile * 4);
+  float* pt = reinterpret_cast<float*>(w);
+  w += al256((size_t)H * rows_c * rows_c * 4);
+  uint8_t* cc = reinterpret_cast<uint8_t*>(w);
+  w += al256((size_t)H * rows_c);
+  double* gs = reinterpret_cast<double*>(w);
+
+  const int n_pool = H * rows_c * kTile;
+  pool_kernel<<<(n_pool + 255) / 256, 256, 0, stream>>>(q, S, H, block, rows_c, pq);
+  pool_kernel<<<(n_pool + 255) / 256, 256, 0, stream>>>(k, S, H, block, rows_c, pk);
+  const int grid_rows = (H * rows_c + kPolWarps - 1) / kPolWarps;
+  const size_t sm_rows = (size_t)kPolWarps * rows_c * 3 * sizeof(double);
+  cudaFuncSetAttribute(scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows);
+  scores_kernel<<<grid_rows, kPolWarps * 32, sm_rows, stream>>>(pq, pk, H, rows_c, pt);
+  const size_t sm_cache = (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2);
+  cudaFuncSetAttribute(cache_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm_cache);
+  cache_select_kernel<<<H, 256, sm_cache, stream>>>(pt, rows_c, n_t, tau_q, s_q, cc, gs);
+  cudaFuncSetAttribute(skip_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows);
+  skip_select_kernel<<<grid_rows, kPolWarps * 32, sm_rows, stream>>>(
+      pt, cc, H, rows_c, n_t, tau_kv, guard, pool_n, t_q, cache_bits, skip_bits);
+  return cudaGetLastError();
+}
+
+}  // namespace fo

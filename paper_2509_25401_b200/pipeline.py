@@ -3,9 +3,9 @@
 Mirrors reference pipeline.py:223-326. update_step refreshes the feature
 cache and the GEMM-O bias and computes the step densely; dispatch_step runs
 the sparse chain GEMM-Q -> sparse attention (mode="bias") -> GEMM-O dispatch
-against the governing update step's symbols. The update-step mask policy
-(policy.py) is not on the GPU yet, so update_step takes the next window's
-symbols from the caller.
+against the governing update step's symbols. The next window's symbols come
+from the GPU mask policy (policy.MaskPolicy, reference policy.py) or from the
+caller.
 
 Multi-GPU: heads are sharded across ranks (shard_heads). GEMM-Q and K/V are
 column-parallel, attention and the cache are per head, GEMM-O is row-parallel
@@ -87,12 +87,19 @@ def _allreduce(out, group):
     return out
 
 
-def update_step(state, x, symbols_next, order_d, *, group=None, check=True):
-    """Refresh cache and bias; compute the step densely (pipeline.py:244-288)."""
+def update_step(state, x, symbols_next, order_d, *, group=None, check=True, policy=None, t=0):
+    """Refresh symbols, cache and bias; compute the step densely
+    (pipeline.py:244-288). The next window's symbols come from `policy`
+    (a MaskPolicy, run on this step's q/k at step t, pipeline.py:254-266)
+    when symbols_next is None, else from the caller."""
     x = as_device(x, torch.bfloat16, "x")
     p = state.params
     q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None)
     k, v = project_kv(x, p)
+    if symbols_next is None:
+        if policy is None:
+            raise ParameterError("update_step needs symbols_next or a MaskPolicy")
+        symbols_next = policy.symbols(q, k, t)
     o = dense_attention_update(q, k, v, state.cache, check=check)
     out, bias = project_out_update(o, p.w_out, symbols_next, state.cache, order_d, check=check)
     state.symbols = symbols_next
