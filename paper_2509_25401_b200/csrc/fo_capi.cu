@@ -41,9 +41,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 row-major [rows, cols] map, box = 64 columns (128 B) x box_rows, SW128
-int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
-             const char* name) {
+// 2-D bf16 row-major [rows, cols] map with a box of box_cols x box_rows
+int make_map_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                uint32_t box_rows, CUtensorMapSwizzle swz, const char* name) {
   auto fn = encode_fn();
   if (!fn) return fail(FO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
@@ -51,13 +51,19 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   if ((cols * 2) % 16 != 0) return fail(FO_ERR_SHAPE, "%s: row pitch not a multiple of 16 B", name);
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FO_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed (%d)", name, (int)r);
   return FO_OK;
+}
+
+// box = 64 columns (128 B) x box_rows, SW128: the MMA operand tiles
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+             const char* name) {
+  return make_map_ex(m, base, rows, cols, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, name);
 }
 
 int g_num_sms = 0;
@@ -325,7 +331,7 @@ int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int s
   p.out = static_cast<__nv_bfloat16*>(out);
   p.bias = static_cast<__nv_bfloat16*>(bias);
   p.status = status;
-  launch_gemm_o(am, cm, wm, p, num_sms(), (cudaStream_t)stream);
+  launch_gemm_o(am, cm, wm, am, p, num_sms(), (cudaStream_t)stream);
   return check_launch("gemm_o_update");
 }
 
@@ -343,7 +349,14 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
   for (int d = 0; d <= order_d; ++d) p.coef[d] = coef[d];
   p.out = static_cast<__nv_bfloat16*>(out);
   p.bias = static_cast<__nv_bfloat16*>(const_cast<void*>(bias));
-  launch_gemm_o(am, cm, wm, p, num_sms(), (cudaStream_t)stream);
+  // epilogue chunks: 128 rows x 32 columns (64 B rows, SW64) of bias and out
+  CUtensorMap bm, om;
+  if ((rc = make_map_ex(&bm, bias, (uint64_t)(order_d + 1) * seq, d_model, 32, 128,
+                        CU_TENSOR_MAP_SWIZZLE_64B, "bias")))
+    return rc;
+  if ((rc = make_map_ex(&om, out, seq, d_model, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B, "out")))
+    return rc;
+  launch_gemm_o(am, bm, wm, om, p, num_sms(), (cudaStream_t)stream);
   return check_launch("gemm_o_dispatch");
 }
 

@@ -27,12 +27,24 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STAGES = 6;
 constexpr int NTHREADS = 256;
 
+// GEMM-O dispatch: one stage fewer, and a ring of bias / output chunks
+// (128 rows x 32 columns, orders 0 and 1, SW64) between the bias-loader warp,
+// the epilogue and the TMA store
+constexpr int D_STAGES = 5;
+constexpr int BIAS_SLOTS = 4;
+constexpr int BIAS_ORDER_BYTES = BM * 32 * 2;  // 8 KB
+constexpr int BIAS_SLOT_BYTES = 2 * BIAS_ORDER_BYTES;
+
 struct Bars {
   uint64_t full[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
+  uint64_t bfull[BIAS_SLOTS], bempty[BIAS_SLOTS];
   uint32_t tmem_base;
 };
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
+constexpr int SMEM_BYTES_D =
+    D_STAGES * STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES + 1024 + (int)sizeof(Bars);
+static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
 __device__ __forceinline__ void init_bars(Bars* b) {
   for (int s = 0; s < STAGES; ++s) {
@@ -43,14 +55,19 @@ __device__ __forceinline__ void init_bars(Bars* b) {
     mbar_init(&b->tfull[a], 1);
     mbar_init(&b->tempty[a], 128);
   }
+  for (int a = 0; a < BIAS_SLOTS; ++a) {
+    mbar_init(&b->bfull[a], 1);
+    mbar_init(&b->bempty[a], 1);
+  }
   fence_barrier_init();
 }
 
 // ring-buffer cursor
+template <int NS = STAGES>
 struct Ring {
   int s = 0, ph = 0;
   __device__ __forceinline__ void next() {
-    if (++s == STAGES) {
+    if (++s == NS) {
       s = 0;
       ph ^= 1;
     }
@@ -123,7 +140,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
 
   if (warp == 0) {
     // TMA producer (whole warp walks the schedule; one elected lane issues)
-    Ring rg;
+    Ring<> rg;
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
       int h, i;
       job(w, h, i);
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     // MMA issuer (warp-uniform schedule, elected lane issues + commits)
     const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
     const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
-    Ring rg;
+    Ring<> rg;
     int t = 0;
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
       const int acc = t & 1;
@@ -264,25 +281,37 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
 // =============================================================================
 // GEMM-O (update: UPDATE=true, dispatch: UPDATE=false)
 // =============================================================================
+// Dispatch epilogue data path: the forecast bias is HBM traffic the size of the
+// output per order, so it moves as TMA tiles, not per-thread row loads (a warp
+// of row-per-thread 16-B loads touches 32 rows = 32 L1 wavefronts). Warp 3
+// streams 128 x 32 bias chunks (orders 0/1, SW64) into a 4-slot ring and pulls
+// the next job's tiles into L2; each epilogue thread reads its row's chunk
+// conflict-free from the swizzled slot, adds the accumulator, writes bf16 back
+// in place and one elected thread TMA-stores the chunk to `out`.
 template <bool UPDATE>
 __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     gemm_o_kernel(const __grid_constant__ CUtensorMap am,  // o   [S, H*128]
-                  const __grid_constant__ CUtensorMap cm,  // diff stacks [(D+1)*S, H*128]
+                  const __grid_constant__ CUtensorMap cm,  // update: diff stacks [(D+1)*S, H*128]
+                                                           // dispatch: bias [(D+1)*S, dm], 32x128 SW64
                   const __grid_constant__ CUtensorMap wm,  // W_out^T [dm, H*128]
+                  const __grid_constant__ CUtensorMap om,  // dispatch: out [S, dm], 32x128 SW64
                   const GemmOParams p) {
   using namespace gemm;
+  constexpr int ST = UPDATE ? STAGES : D_STAGES;
   constexpr int ACC_COLS = UPDATE ? 2 * BN : BN;  // update: accumulator A (active) + B (cached)
   constexpr int TM_COLS = UPDATE ? 512 : 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* ring = smem + ST * STAGE_BYTES;  // dispatch bias / output chunks
+  Bars* bars = reinterpret_cast<Bars*>(ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES));
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     init_bars(bars);
     tma_prefetch_desc(&am);
     tma_prefetch_desc(&cm);
     tma_prefetch_desc(&wm);
+    if (!UPDATE) tma_prefetch_desc(&om);
   }
   if (warp == 2) tmem_alloc<TM_COLS>(&bars->tmem_base);
   tc_fence_before();
@@ -304,10 +333,13 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     i = rest / nbn;
     return !(UPDATE && d > 0 && d >= p.orders[i]);
   };
+  // dispatch: bias orders staged through the ring for block i (orders >= 2 are
+  // rare and read directly)
+  auto staged_orders = [&](int i) { return min(min(p.order_d + 1, p.orders[i]), 2); };
 
   if (warp == 0) {
     {
-      Ring rg;
+      Ring<ST> rg;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
         int i, nb, d;
         if (!job(w, i, nb, d)) continue;
@@ -343,7 +375,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     {
       const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
       const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
-      Ring rg;
+      Ring<ST> rg;
       int t = 0;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
         int i, nb, d;
@@ -378,112 +410,173 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       }
     }
     __syncwarp();
+  } else if (!UPDATE && warp == 3) {
+    // bias loader: 4 chunks per job through the slot ring, next job prefetched into L2
+    Ring<BIAS_SLOTS> rb;
+    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+      const int nb = w % nbn, i = w / nbn;
+      const int ns = staged_orders(i);
+      const int wn = w + gridDim.x;
+      if (wn < n_jobs && elect_one()) {
+        const int nb2 = wn % nbn, i2 = wn / nbn;
+        const int ns2 = staged_orders(i2);
+        for (int dd = 0; dd < ns2; ++dd)
+          for (int c = 0; c < 4; ++c) tma_prefetch_l2_2d(&cm, nb2 * BN + c * 32, dd * p.S + i2 * BM);
+      }
+      __syncwarp();
+      for (int c = 0; c < 4; ++c) {
+        mbar_wait(&bars->bempty[rb.s], rb.ph ^ 1);
+        if (elect_one()) {
+          uint8_t* slot = ring + rb.s * BIAS_SLOT_BYTES;
+          mbar_arrive_expect_tx(&bars->bfull[rb.s], ns * BIAS_ORDER_BYTES);
+          for (int dd = 0; dd < ns; ++dd)
+            tma_load_2d(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s], nb * BN + c * 32,
+                        dd * p.S + i * BM);
+        }
+        __syncwarp();
+        rb.next();
+      }
+    }
   } else if (warp >= 4) {
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const size_t SD = (size_t)p.S * p.dm;
-    int t = 0;
-    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
-      int i, nb, d;
-      if (!job(w, i, nb, d)) continue;
-      const int acc = t & 1;
-      const unsigned long long act = p.hmask[i];
-      const unsigned long long cached = all_heads & ~act;
-      const bool hasA = (d == 0) && act != 0ull;
-      const bool hasB = UPDATE && cached != 0ull;
-      const int no = UPDATE ? 0 : min(p.order_d + 1, p.orders[i]);
-      const int row = i * BM + r;
-      const bool row_ok = row < p.S;
-      const size_t obase = (size_t)row * p.dm + (size_t)nb * BN;
-      // dispatch: this thread's bias row segment (orders 0..1, 128 columns) is
-      // fetched into registers before the accumulator wait, so the HBM latency
-      // overlaps the mainloop instead of stalling each 32-column chunk; the next
-      // tile's rows are pulled into L2 meanwhile
-      uint4 bv[2][16];
-      if (!UPDATE) {
+    if constexpr (UPDATE) {
+      int t = 0;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+        int i, nb, d;
+        if (!job(w, i, nb, d)) continue;
+        const int acc = t & 1;
+        const unsigned long long act = p.hmask[i];
+        const unsigned long long cached = all_heads & ~act;
+        const bool hasA = (d == 0) && act != 0ull;
+        const bool hasB = cached != 0ull;
+        const int row = i * BM + r;
+        const bool row_ok = row < p.S;
+        const size_t obase = (size_t)row * p.dm + (size_t)nb * BN;
+        mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
+        const uint32_t tB = tA + BN;
 #pragma unroll
-        for (int dd = 0; dd < 2; ++dd)
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ua[32], ub[32];
+          if (hasA) tmem_ld32(tA + c * 32, ua);
+          if (hasB) tmem_ld32(tB + c * 32, ub);
+          tmem_ld_wait();
+          gemm::reg_fence(ua);
+          gemm::reg_fence(ub);
+          if (!row_ok) continue;
+          float o[32], b[32];
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            bv[dd][q] = (row_ok && dd < no)
-                            ? __ldg(reinterpret_cast<const uint4*>(p.bias + dd * SD + obase) + q)
-                            : make_uint4(0u, 0u, 0u, 0u);
-        const int wn = w + gridDim.x;
-        if (wn < n_jobs) {
-          const int i2 = wn / nbn, nb2 = wn % nbn;
-          const int row2 = i2 * BM + r;
-          const int no2 = min(p.order_d + 1, p.orders[i2]);
-          if (row2 < p.S)
-            for (int dd = 0; dd < no2; ++dd) {
-              const __nv_bfloat16* a = p.bias + dd * SD + (size_t)row2 * p.dm + (size_t)nb2 * BN;
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 64));
-            }
-        }
-      }
-      const float c0 = p.coef[0], c1 = p.coef[1];
-      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
-      tc_fence_after();
-      const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
-      const uint32_t tB = tA + (UPDATE ? BN : 0);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t ua[32], ub[32];
-        if (hasA) tmem_ld32(tA + c * 32, ua);
-        if (UPDATE && hasB) tmem_ld32(tB + c * 32, ub);
-        tmem_ld_wait();
-        gemm::reg_fence(ua);
-        gemm::reg_fence(ub);
-        float o[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) o[k] = hasA ? __uint_as_float(ua[k]) : 0.f;
-        if (!row_ok) continue;
-        if (UPDATE) {
-          float b[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) b[k] = hasB ? __uint_as_float(ub[k]) : 0.f;
+          for (int k = 0; k < 32; ++k) {
+            o[k] = hasA ? __uint_as_float(ua[k]) : 0.f;
+            b[k] = hasB ? __uint_as_float(ub[k]) : 0.f;
+          }
           if (d == 0) {
 #pragma unroll
             for (int k = 0; k < 32; ++k) o[k] += b[k];
             gemm::store_bf16x32(p.out + obase + c * 32, o);
           }
           if (hasB && p.orders[i] > d) gemm::store_bf16x32(p.bias + d * SD + obase + c * 32, b);
-        } else {
+        }
+        tc_fence_before();
+        mbar_arrive(&bars->tempty[acc]);
+        ++t;
+      }
+    } else {
+      const float c0 = p.coef[0], c1 = p.coef[1], c2 = p.coef[2], c3 = p.coef[3];
+      const uint32_t ring_u32 = smem_u32(ring);
+      const int sw = (r >> 1) & 3;  // SW64: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
+      Ring<BIAS_SLOTS> rb;
+      int prev = -1;  // slot of the previous chunk (released once its store has read it)
+      int t = 0;
+      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+        const int nb = w % nbn, i = w / nbn;
+        const int acc = t & 1;
+        const bool hasA = p.hmask[i] != 0ull;
+        const int no = min(p.order_d + 1, p.orders[i]);
+        const int ns = min(no, 2);
+        const int row = i * BM + r;
+        const bool row_ok = row < p.S;
+        mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ua[32];
+          if (hasA) {
+            tmem_ld32(tA + c * 32, ua);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int dd = 0; dd < 2; ++dd) {
-            const float cf = dd == 0 ? c0 : c1;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 b4 = bv[dd][c * 4 + q];
-              const uint32_t w4[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {  // zero-filled when dd >= no
-                o[q * 8 + 2 * e] = fmaf(cf, bf16lo(w4[e]), o[q * 8 + 2 * e]);
-                o[q * 8 + 2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[q * 8 + 2 * e + 1]);
-              }
-            }
+            for (int k = 0; k < 32; ++k) ua[k] = 0u;
           }
-          for (int dd = 2; dd < no; ++dd) {  // orders 2..3 (rare): direct loads
-            const uint4* bsrc = reinterpret_cast<const uint4*>(p.bias + dd * SD + obase + c * 32);
-            const float cf = p.coef[dd];
+          if (c == 3) {  // accumulator drained: release it to the MMA warp
+            tc_fence_before();
+            mbar_arrive(&bars->tempty[acc]);
+          }
+          mbar_wait(&bars->bfull[rb.s], rb.ph);
+          const uint32_t rowa = ring_u32 + rb.s * BIAS_SLOT_BYTES + r * 64;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 b4 = __ldg(bsrc + q);
-              const uint32_t w4[4] = {b4.x, b4.y, b4.z, b4.w};
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t a = rowa + ((q ^ sw) << 4);
+            float o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = __uint_as_float(ua[q * 8 + k]);
+            if (ns > 0) {
+              const uint4 b = lds128(a);
+              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                o[q * 8 + 2 * e] = fmaf(cf, bf16lo(w4[e]), o[q * 8 + 2 * e]);
-                o[q * 8 + 2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[q * 8 + 2 * e + 1]);
+                o[2 * e] = fmaf(c0, bf16lo(w4[e]), o[2 * e]);
+                o[2 * e + 1] = fmaf(c0, bf16hi(w4[e]), o[2 * e + 1]);
               }
             }
+            if (ns > 1) {
+              const uint4 b = lds128(a + BIAS_ORDER_BYTES);
+              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[2 * e] = fmaf(c1, bf16lo(w4[e]), o[2 * e]);
+                o[2 * e + 1] = fmaf(c1, bf16hi(w4[e]), o[2 * e + 1]);
+              }
+            }
+            for (int dd = 2; dd < no; ++dd) {  // orders 2..3 (rare): direct loads
+              if (!row_ok) break;
+              const float cf = dd == 2 ? c2 : c3;
+              const uint4 b = __ldg(reinterpret_cast<const uint4*>(
+                  p.bias + dd * SD + (size_t)row * p.dm + (size_t)nb * BN + c * 32 + q * 8));
+              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[2 * e] = fmaf(cf, bf16lo(w4[e]), o[2 * e]);
+                o[2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[2 * e + 1]);
+              }
+            }
+            sts128(a, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                 pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7])));
           }
-          gemm::store_bf16x32(p.out + obase + c * 32, o);
+          fence_proxy_async();
+          named_bar_sync(1, 128);
+          if (warp == 4) {
+            if (elect_one()) {
+              tma_store_2d(&om, ring + rb.s * BIAS_SLOT_BYTES, nb * BN + c * 32, i * BM);
+              bulk_commit();
+              bulk_wait_read<1>();  // the previous chunk's store has read its slot
+              if (prev >= 0) mbar_arrive(&bars->bempty[prev]);
+            }
+            __syncwarp();
+          }
+          prev = rb.s;
+          rb.next();
         }
+        ++t;
       }
-      tc_fence_before();
-      mbar_arrive(&bars->tempty[acc]);
-      ++t;
+      if (warp == 4) {
+        if (elect_one()) bulk_wait<0>();
+        __syncwarp();
+      }
     }
   }
   tc_fence_before();
@@ -506,19 +599,19 @@ void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQPara
 }
 
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
-                   const GemmOParams& p, int grid, cudaStream_t stream) {
+                   const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(gemm_o_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          gemm::SMEM_BYTES);
     cudaFuncSetAttribute(gemm_o_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm::SMEM_BYTES);
+                         gemm::SMEM_BYTES_D);
     configured = true;
   }
   if (p.update)
-    gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, p);
+    gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, om, p);
   else
-    gemm_o_kernel<false><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, p);
+    gemm_o_kernel<false><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES_D, stream>>>(am, cm, wm, om, p);
 }
 
 }  // namespace fo

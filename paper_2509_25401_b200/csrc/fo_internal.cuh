@@ -104,7 +104,7 @@ struct GemmOParams {
   uint32_t* status;
 };
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
-                   const GemmOParams& p, int grid, cudaStream_t stream);
+                   const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream);
 
 // elementwise helpers
 void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,

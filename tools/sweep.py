@@ -124,17 +124,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--parts", default="attn,flux,gemm", help="subset of attn,flux,gemm")
     a = ap.parse_args()
+    parts = set(a.parts.split(","))
     pts = [("dense", 0.0, 0.0)]
     pts += [("FC", c, 0.0) for c in (0.1, 0.3, 0.5, 0.8)]
     pts += [("BSS", 0.0, s) for s in (0.1, 0.3, 0.5, 0.8)]
     pts += [("FC+BSS", c, s) for c, s in ((0.25, 0.5), (0.5, 0.6), (0.5, 0.8))]
-    res = {"device": torch.cuda.get_device_name(), "attention_c4": attention_sweep(33024, 24, pts)}
+    res = {"device": torch.cuda.get_device_name()}
+    if "attn" in parts:
+        res["attention_c4"] = attention_sweep(33024, 24, pts)
     flux = [("BSS", 0.0, s) for s in (0.0, 0.1, 0.3, 0.5, 0.7, 0.9)]
-    res["attention_c2_flux"] = attention_sweep(4608, 24, flux)
+    if "flux" in parts:
+        res["attention_c2_flux"] = attention_sweep(4608, 24, flux)
     ratios = (0.0, 0.25, 0.5, 0.75, 0.9)
-    res["gemm_c3_s4096_D1"] = gemm_sweep(4096, 24, 3072, ratios, order=1)
-    if not a.quick:
+    if "gemm" in parts:
+        res["gemm_c3_s4096_D1"] = gemm_sweep(4096, 24, 3072, ratios, order=1)
+    if "gemm" in parts and not a.quick:
         res["gemm_c3_s33024_D1"] = gemm_sweep(33024, 24, 3072, ratios, order=1)
         res["gemm_c3_s33024_D0"] = gemm_sweep(33024, 24, 3072, ratios, order=0)
     txt = json.dumps(res, indent=1)
