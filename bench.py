@@ -393,7 +393,9 @@ def run_b200(args, cfg, rank, world):
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": sustained,
                      "unit": "TFLOP/s", "frac": round(ach / sustained, 4), "traffic": traffic,
-                     "kernel": "sparse_attention_kernel", "peak_source": f"{src} bf16 sustained",
+                     "kernel": ("sparse_attention_kernel" if os.environ.get("FO_ATTN_IMPL") == "v1"
+                                else "sparse_attention_cs_kernel"),
+                     "peak_source": f"{src} bf16 sustained",
                      "algorithmic_flops_per_launch": attn_flops},
     }
     if "dense_ms" in res:

@@ -8,8 +8,8 @@ import subprocess
 import sys
 
 HERE = pathlib.Path(__file__).resolve().parent
-SOURCES = ["fo_symbols.cu", "fo_attention.cu", "fo_gemm.cu", "fo_elementwise.cu", "fo_policy.cu",
-           "fo_capi.cu"]
+SOURCES = ["fo_symbols.cu", "fo_attention.cu", "fo_attention_cs.cu", "fo_gemm.cu",
+           "fo_elementwise.cu", "fo_policy.cu", "fo_capi.cu"]
 OUT = HERE / "_fo_b200.so"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,496 @@
+// K2 / K2u, column-split softmax (sm_100a): the default attention kernel.
+//
+// Same contract and pipeline as fo_attention.cu (reference attention.py:150-221
+// with the tile kernel pyref.py:14-48): producer warp, MMA warp with a
+// double-buffered S in TMEM and P read straight from TMEM by the PV MMA. The
+// softmax differs: two warpgroups share every tile, warp w (4..7) taking key
+// columns 0-63 and warp w+4 (8..11) columns 64-127 of the same 32 rows (the
+// same TMEM lane quarter, hence the same SMSP).
+//
+// Why (tools/softmax_microbench.cu, ncu): the 128x128 tile softmax costs ~1340
+// cycles per SMSP with one warp, which cannot cover its own dependency
+// latencies, and ~1030 with two. Splitting columns puts two warps on every
+// SMSP while keeping the S double buffer, so QK(j+1) still overlaps softmax(j).
+// The two-stream ping-pong alternative serialises each stream's
+// S -> P -> PV -> S chain and measured 20% slower. The partners exchange
+// half-row maxima through shared memory behind a 64-thread named barrier, so
+// both apply the same running max. Each writes its half of P (P columns 0-31 /
+// 32-63, after both have read S) and rescales its half of O. Row sums are fp32
+// in registers, combined once per item: the P x ones row-sum MMA of
+// fo_attention.cu re-reads P from TMEM and costs ~512 tensor cycles per tile.
+#include "fo_internal.cuh"
+
+// pairs (of every 8) whose exp2 runs as the FMA-pipe polynomial; with two
+// softmax warps per SMSP the MUFU is the tighter pipe, so more go to the FMA
+#ifndef FO_CS_POLY_OF_8
+#define FO_CS_POLY_OF_8 3
+#endif
+// 1: row sums by a P x ones MMA into TMEM (re-reads P from TMEM: ~512 tensor
+// cycles per tile); 0: fp32 row sums in registers, halves combined per item
+#ifndef FO_CS_TC_ROWSUM
+#define FO_CS_TC_ROWSUM 0
+#endif
+
+namespace fo {
+namespace attn_cs {
+constexpr int KST = 3, VST = 2;
+constexpr int TILE_BYTES = kTile * kTile * 2;  // 32 KB bf16 tile
+constexpr int HALF_BYTES = TILE_BYTES / 2;     // 128 rows x 64 cols, 128B-swizzled
+constexpr int SMEM_TILES = 1 + KST + VST;
+constexpr int NTHREADS = 384;
+constexpr int SOFTMAX_THREADS = 256;
+constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
+constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (B operand of the row-sum MMA)
+
+struct Bars {
+  uint64_t q_full, q_empty;
+  uint64_t k_full[KST], k_empty[KST];
+  uint64_t v_full[VST], v_empty[VST];
+  uint64_t s_full[2];
+  uint64_t p_full, o_done, o_last, o_free;
+  uint32_t tmem_base;
+  float xmax[2][2][128];  // [tile parity][column half][row]: half-row maxima
+  float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
+};
+constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
+static_assert(SMEM_BYTES <= 232448, "column-split attention exceeds shared memory");
+}  // namespace attn_cs
+
+namespace {
+template <int N>
+__device__ __forceinline__ void reg_fence_cs(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) asm volatile("" : "+r"(r[k]));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
+    sparse_attention_cs_kernel(const __grid_constant__ CUtensorMap qm,
+                               const __grid_constant__ CUtensorMap km,
+                               const __grid_constant__ CUtensorMap vm, const AttnParams p) {
+  using namespace attn_cs;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TILE_BYTES;
+  uint8_t* sV = smem + TILE_BYTES * (1 + KST);
+  uint8_t* sOnes = smem + TILE_BYTES * SMEM_TILES;  // 1024-aligned
+  Bars* bars = reinterpret_cast<Bars*>(sOnes + ONES_BYTES);
+  for (int e = threadIdx.x; e < ONES_BYTES / 4; e += blockDim.x)
+    reinterpret_cast<uint32_t*>(sOnes)[e] = 0x3F803F80u;  // bf16 1.0 pairs
+  fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+  const int warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&bars->k_full[s], 1);
+      mbar_init(&bars->k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&bars->v_full[s], 1);
+      mbar_init(&bars->v_empty[s], 1);
+    }
+    mbar_init(&bars->s_full[0], 1);
+    mbar_init(&bars->s_full[1], 1);
+    mbar_init(&bars->p_full, SOFTMAX_THREADS / 32);  // one arrival per softmax warp
+    mbar_init(&bars->o_done, 1);
+    mbar_init(&bars->o_last, 1);
+    mbar_init(&bars->o_free, SOFTMAX_THREADS);
+    fence_barrier_init();
+    tma_prefetch_desc(&qm);
+    tma_prefetch_desc(&km);
+    tma_prefetch_desc(&vm);
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+  const int n_items = *p.n_items;
+  const size_t head_sym = (size_t)p.comp_rows * p.row_stride;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+      const int2 it = p.items[w];
+      const int h = it.x >> 20, i = it.x & 0xFFFFF;
+      mbar_wait(&bars->q_empty, (qi & 1) ^ 1, p.status);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
+        tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, i * kTile);
+        tma_load_2d(sQ + HALF_BYTES, &qm, &bars->q_full, h * kTile + 64, i * kTile);
+      }
+      __syncwarp();
+      const uint8_t* sym = p.s_s + h * head_sym;
+      for (int base = 0; base < p.t_kv; base += 32) {
+        const int j = base + lane;
+        const uint32_t bit =
+            (j < p.t_kv) && (p.dense || decode_reduction(sym, p.row_stride, i, j, p.pool_n));
+        uint32_t m = __ballot_sync(0xffffffffu, bit);  // warp-uniform
+        while (m) {
+          const int jj = base + __ffs(m) - 1;
+          m &= m - 1;
+          mbar_wait(&bars->k_empty[kst], kph ^ 1, p.status);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&bars->k_full[kst], TILE_BYTES);
+            uint8_t* dk = sK + kst * TILE_BYTES;
+            tma_load_2d(dk, &km, &bars->k_full[kst], h * kTile, jj * kTile);
+            tma_load_2d(dk + HALF_BYTES, &km, &bars->k_full[kst], h * kTile + 64, jj * kTile);
+          }
+          __syncwarp();
+          if (++kst == KST) {
+            kst = 0;
+            kph ^= 1;
+          }
+          mbar_wait(&bars->v_empty[vst], vph ^ 1, p.status);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
+            uint8_t* dv = sV + vst * TILE_BYTES;
+            tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
+            tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
+          }
+          __syncwarp();
+          if (++vst == VST) {
+            vst = 0;
+            vph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    {
+      const uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
+      const uint32_t idesc_pv = make_idesc_bf16(128, 128, false, true);
+      const uint32_t idesc_l = make_idesc_bf16(128, 16, false, false);
+      const uint64_t ones_desc = make_sdesc_sw128(smem_u32(sOnes), 16, 1024);
+      (void)idesc_l;
+      (void)ones_desc;
+      int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
+      uint32_t qk_cnt = 0, pv_cnt = 0;
+      const uint64_t qdesc = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t kdesc0 = make_sdesc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t vdesc0 = make_sdesc_sw128(smem_u32(sV), HALF_BYTES, 1024);
+      auto issue_qk = [&]() {
+        mbar_wait(&bars->k_full[kst], kph, p.status);
+        tc_fence_after();
+        const uint32_t sb = qk_cnt & 1;
+        const uint32_t d = tbase + TM_S0 + sb * 128;
+        const uint64_t kdesc = kdesc0 + (uint64_t)((kst * TILE_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t off = (uint64_t)((k >> 2) * (HALF_BYTES >> 4) + (k & 3) * 2);
+            mma_bf16_ss(d, qdesc + off, kdesc + off, idesc_qk, k > 0);
+          }
+          tc_commit(&bars->k_empty[kst]);
+          tc_commit(&bars->s_full[sb]);
+        }
+        __syncwarp();
+        if (++kst == KST) {
+          kst = 0;
+          kph ^= 1;
+        }
+        ++qk_cnt;
+      };
+      auto commit_q_empty = [&]() {
+        if (elect_one()) tc_commit(&bars->q_empty);
+        __syncwarp();
+      };
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+        const int n = p.items[w].y;
+        mbar_wait(&bars->q_full, qi & 1, p.status);
+        tc_fence_after();
+        issue_qk();
+        if (n == 1) commit_q_empty();
+        for (int j = 0; j < n; ++j) {
+          if (j + 1 < n) {
+            issue_qk();
+            if (j + 2 == n) commit_q_empty();
+          }
+          mbar_wait(&bars->p_full, pv_cnt & 1, p.status);
+          if (j == 0 && qi > 0) mbar_wait(&bars->o_free, (qi - 1) & 1, p.status);
+          mbar_wait(&bars->v_full[vst], vph, p.status);
+          tc_fence_after();
+          const uint32_t a_t = tbase + TM_S0 + (pv_cnt & 1) * 128;
+          const uint64_t vdesc = vdesc0 + (uint64_t)((vst * TILE_BYTES) >> 4);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              mma_bf16_ts(tbase + TM_O, a_t + k * 8, vdesc + (uint64_t)(k * (2048 >> 4)), idesc_pv,
+                          (j > 0 || k > 0));
+#if FO_CS_TC_ROWSUM
+            // row sums on the tensor core: L += P . 1, so l is exactly sum(bf16(P))
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              mma_bf16_ts(tbase + TM_L, a_t + k * 8, ones_desc, idesc_l, (j > 0 || k > 0));
+#endif
+            tc_commit(&bars->v_empty[vst]);
+            tc_commit(&bars->o_done);
+            if (j == n - 1) tc_commit(&bars->o_last);
+          }
+          __syncwarp();
+          if (++vst == VST) {
+            vst = 0;
+            vph ^= 1;
+          }
+          ++pv_cnt;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------- softmax + epilogue (half rows)
+    const int half = (warp >= 8) ? 1 : 0;  // key columns [64*half, 64*half + 64)
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const int last_valid = p.S - (p.t_kv - 1) * kTile;  // valid key columns of the last block
+    const int col0 = half * 64;
+    const size_t HD = (size_t)p.H * kTile;
+    const size_t stack_stride = (size_t)p.S * HD;
+    const int pair_bar = 1 + q4;  // named barrier of warps (q4 + 4, q4 + 8)
+    const uint32_t xmax_u32 = smem_u32(&bars->xmax[0][0][0]);
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    uint32_t qk_seen = 0, o_base = 0;
+    int qi = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+      const int2 it = p.items[w];
+      const int h = it.x >> 20, i = it.x & 0xFFFFF, n = it.y;
+      const bool tail = (last_valid < kTile) &&
+                        (p.dense || decode_reduction(p.s_s + h * head_sym, p.row_stride, i,
+                                                     p.t_kv - 1, p.pool_n));
+      const int valid_old = (p.cache && p.valid) ? p.valid[(size_t)h * p.t_q + i] : 0;
+      float m_run = -INFINITY;
+      float2 l2 = make_float2(0.f, 0.f);
+      for (int j = 0; j < n; ++j) {
+        const uint32_t sb = qk_seen & 1;
+        mbar_wait(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
+        tc_fence_after();
+        const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
+        uint32_t u[2][32];
+        tmem_ld32(sa + col0, u[0]);
+        tmem_ld32(sa + col0 + 32, u[1]);
+        tmem_ld_wait();
+        reg_fence_cs(u[0]);
+        reg_fence_cs(u[1]);
+        const bool mask_tail = tail && (j == n - 1);
+        float sv[64];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) sv[c * 32 + k] = __uint_as_float(u[c][k]);
+        if (mask_tail) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k)
+            if (col0 + k >= last_valid) sv[k] = -INFINITY;
+        }
+        // half-row max: four FMNMX3 chains of 16, then exchange with the partner warp
+        float mc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float a = fmax3f(sv[16 * c], sv[16 * c + 1], sv[16 * c + 2]);
+#pragma unroll
+          for (int k = 3; k < 15; k += 2) a = fmax3f(a, sv[16 * c + k], sv[16 * c + k + 1]);
+          mc[c] = fmaxf(a, sv[16 * c + 15]);
+        }
+        const float mh = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
+        const uint32_t xa = xmax_u32 + (((qk_seen & 1) * 2) * 128 + r) * 4;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xa + half * 512), "f"(mh) : "memory");
+        // both partners have read their S halves before either overwrites S with P
+        named_bar_sync(pair_bar, 64);
+        float mo;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(mo) : "r"(xa + (half ^ 1) * 512) : "memory");
+        ++qk_seen;
+        const float m_tile = fmaxf(mh, mo) * p.scale_log2;
+        bool need = false;
+        float m_new;
+        if (j == 0) {
+          m_new = m_tile;
+        } else if (m_tile > m_run + 8.f) {
+          need = true;
+          m_new = m_tile;
+        } else {
+          m_new = m_run;
+        }
+        const float corr = need ? fast_exp2(m_run - m_new) : 1.f;
+        m_run = m_new;
+        l2.x *= corr;  // the running sum moves to the new max before this tile adds to it
+        l2.y *= corr;
+        const float2 nm2 = make_float2(-m_new, -m_new);
+        uint32_t pk[32];
+        if (!mask_tail) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
+            float2 e;
+            if ((q & 7) < FO_CS_POLY_OF_8) {
+              e = exp2_poly2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
+            }
+            if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
+            pk[q] = pack_bf16x2(e.x, e.y);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
+            const float2 e = make_float2(fast_exp2(x.x), fast_exp2(x.y));  // exact zeros when masked
+            if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
+            pk[q] = pack_bf16x2(e.x, e.y);
+          }
+        }
+        tmem_st32(sa + half * 32, pk);
+        tmem_st_wait();
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)
+          mbar_wait(&bars->o_done, (o_base + j - 1) & 1, p.status);
+          tc_fence_after();
+          const uint32_t oa = tbase + lane_off + TM_O + col0;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {  // this half of O
+            uint32_t o[32];
+            tmem_ld32(oa + c * 32, o);
+            tmem_ld_wait();
+            reg_fence_cs(o);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * corr);
+            tmem_st32(oa + c * 32, o);
+          }
+          if (FO_CS_TC_ROWSUM && half == 0) {  // and the row-sum columns
+            uint32_t l16[16];
+            tmem_ld16(tbase + lane_off + TM_L, l16);
+            tmem_ld_wait();
+            reg_fence_cs(l16);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) l16[k] = __float_as_uint(__uint_as_float(l16[k]) * corr);
+            tmem_st16(tbase + lane_off + TM_L, l16);
+          }
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();  // every lane's P / O stores are complete (tcgen05.wait::st above)
+        if (lane == 0) mbar_arrive(&bars->p_full);
+      }
+      // ---------------- epilogue: this half of O / l -> bf16 -> HBM (+ cache push)
+      mbar_wait(&bars->o_last, qi & 1, p.status);
+      o_base += n;
+      tc_fence_after();
+      float l_row;
+      if (FO_CS_TC_ROWSUM) {
+        uint32_t lsum[16];
+        tmem_ld16(tbase + lane_off + TM_L, lsum);
+        tmem_ld_wait();
+        reg_fence_cs(lsum);
+        l_row = __uint_as_float(lsum[0]);
+      } else {
+        // combine the two halves' partial sums (both scaled by the same maxima)
+        bars->xsum[half][r] = l2.x + l2.y;
+        named_bar_sync(pair_bar, 64);
+        l_row = bars->xsum[0][r] + bars->xsum[1][r];
+      }
+      const float inv_l = 1.f / l_row;
+      const int row = i * kTile + r;
+      const bool row_ok = row < p.S;
+      const int vn = min(valid_old + 1, p.order_d + 1);
+      const uint32_t oa = tbase + lane_off + TM_O + col0;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t o[32];
+        tmem_ld32(oa + c * 32, o);
+        tmem_ld_wait();
+        reg_fence_cs(o);
+        float of[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) of[k] = __uint_as_float(o[k]) * inv_l;
+        if (row_ok) {
+          const size_t off = (size_t)row * HD + (size_t)h * kTile + col0 + c * 32;
+          uint4* dst = reinterpret_cast<uint4*>(p.out + off);
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            uint4 pkv;
+            pkv.x = pack_bf16x2(of[v4 * 8 + 0], of[v4 * 8 + 1]);
+            pkv.y = pack_bf16x2(of[v4 * 8 + 2], of[v4 * 8 + 3]);
+            pkv.z = pack_bf16x2(of[v4 * 8 + 4], of[v4 * 8 + 5]);
+            pkv.w = pack_bf16x2(of[v4 * 8 + 6], of[v4 * 8 + 7]);
+            dst[v4] = pkv;
+          }
+          if (p.cache) {
+            // backward-difference push: new[0]=o, new[d]=new[d-1]-old[d-1] for d<vn, else 0
+            float cur[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) cur[k] = of[k];
+            for (int d = 0; d <= p.order_d; ++d) {
+              uint4* cd = reinterpret_cast<uint4*>(p.cache + d * stack_stride + off);
+              float nxt[32];
+              const bool live_next = (d + 1 < vn);
+              if (live_next) {
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) {
+                  uint4 ov = cd[v4];
+                  const uint32_t w4[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    nxt[v4 * 8 + 2 * e] = cur[v4 * 8 + 2 * e] - bf16lo(w4[e]);
+                    nxt[v4 * 8 + 2 * e + 1] = cur[v4 * 8 + 2 * e + 1] - bf16hi(w4[e]);
+                  }
+                }
+              }
+              const bool live = d < vn;
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4) {
+                uint4 pkv;
+                if (live) {
+                  pkv.x = pack_bf16x2(cur[v4 * 8 + 0], cur[v4 * 8 + 1]);
+                  pkv.y = pack_bf16x2(cur[v4 * 8 + 2], cur[v4 * 8 + 3]);
+                  pkv.z = pack_bf16x2(cur[v4 * 8 + 4], cur[v4 * 8 + 5]);
+                  pkv.w = pack_bf16x2(cur[v4 * 8 + 6], cur[v4 * 8 + 7]);
+                } else {
+                  pkv = make_uint4(0, 0, 0, 0);
+                }
+                cd[v4] = pkv;
+              }
+              if (live_next) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) cur[k] = nxt[k];
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->o_free);
+      if (r == 0 && half == 0) {
+        if (p.pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
+                               static_cast<unsigned long long>(n));
+        if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
+                         const AttnParams& p, int grid, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(sparse_attention_cs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         attn_cs::SMEM_BYTES);
+    configured = true;
+  }
+  sparse_attention_cs_kernel<<<grid, attn_cs::NTHREADS, attn_cs::SMEM_BYTES, stream>>>(qm, km, vm,
+                                                                                     p);
+}
+
+}  // namespace fo

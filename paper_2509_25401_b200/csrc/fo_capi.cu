@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/flashomni_b200.h"
@@ -64,6 +65,18 @@ int make_map_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, 
 int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
              const char* name) {
   return make_map_ex(m, base, rows, cols, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, name);
+}
+
+// Attention kernel: the column-split softmax kernel (fo_attention_cs.cu) by
+// default; FO_ATTN_IMPL=v1 selects the single-warpgroup one (read once per
+// process; both meet the same parity tests)
+int attention_impl() {
+  static int impl = -1;
+  if (impl < 0) {
+    const char* e = getenv("FO_ATTN_IMPL");
+    impl = (e && strcmp(e, "v1") == 0) ? 0 : 1;
+  }
+  return impl;
 }
 
 int g_num_sms = 0;
@@ -223,7 +236,10 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
   fo_dbg_ptr = g_dbg;
 #endif
   if (!update_mode && !s_s) return fail(FO_ERR_PARAM, "s_s is NULL");
-  launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
+  if (attention_impl() == 1)
+    launch_attention_cs(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
+  else
+    launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
   return check_launch("sparse_attention");
 }
 

@@ -76,6 +76,9 @@ struct AttnParams {
 
 void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                       const AttnParams& p, int grid, cudaStream_t stream);
+// two softmax warpgroups splitting every tile's key columns (fo_attention_cs.cu)
+void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
+                         const AttnParams& p, int grid, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // GEMMs
