@@ -42,7 +42,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
@@ -96,24 +96,39 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
 
+    def _rows(self):
+        self.f.flush()
+        try:
+            return [r for r in open(self.f.name).read().splitlines() if r.strip()]
+        except OSError:
+            return []
+
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
-        time.sleep(0.3)
+        # nvidia-smi can take seconds to start: wait for its first sample so the
+        # samples taken from here on cover the timed region
+        t0 = time.time()
+        while self.p is not None and not self._rows() and time.time() - t0 < 15:
+            time.sleep(0.05)
+        self.mark = max(len(self._rows()) - 1, 0)
         return self
 
     def __exit__(self, *a):
         if self.p is not None:
+            # one more sample taken at/after the end of the timed region
+            n, t0 = len(self._rows()), time.time()
+            while len(self._rows()) <= n and time.time() - t0 < 2:
+                time.sleep(0.01)
             self.p.terminate()
             self.p.wait()
 
     def summary(self):
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        rows = [r.split(",") for r in self._rows()[getattr(self, "mark", 0):]]
         os.unlink(self.f.name)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}

@@ -22,6 +22,7 @@ from omniattn import gemm as ref_gemm  # noqa: E402
 from omniattn import symbols as ref_sym  # noqa: E402
 from omniattn import policy as ref_policy  # noqa: E402
 from omniattn import verify as ref_verify  # noqa: E402
+from omniattn import pipeline as ref_pipeline  # noqa: E402
 
 OUT = pathlib.Path(__file__).resolve().parents[1] / "tests" / "golden"
 T = 128
@@ -186,8 +187,71 @@ def policy():
     np.savez_compressed(OUT / "policy.npz", **d)
 
 
+# run() configurations (pipeline.py:337-371) at the sm_100a tile geometry
+RUN_CASES = [
+    dict(n_text=128, n_vision=896, d_model=128, heads=2, tau_q=0.3, tau_kv=0.4, interval_n=3,
+         order_d=1, steps=6, layers=2, workload="drift", smoothness=0.05, seed=7),
+    dict(n_text=200, n_vision=1848, d_model=128, heads=2, pool_n=2, tau_q=0.8, tau_kv=0.7,
+         interval_n=3, order_d=0, steps=6, layers=1, warmup=4, workload="poly2", smoothness=0.1,
+         seed=8),
+]
+STEP_KEYS = ("attn_pairs_total", "attn_pairs_computed", "attn_pairs_mask_skipped",
+             "gemm_q_macs_dense", "gemm_q_macs_actual", "gemm_o_macs_dense", "gemm_o_macs_actual",
+             "gemm_o_bias_macs")
+
+
+class _Bf16Workload:
+    """The reference SyntheticWorkload with its projection weights and every
+    x(t) rounded to bf16 (norm weights stay fp32, as on the GPU), so the GPU
+    engine and the reference consume identical numbers."""
+
+    def __init__(self, cfg):
+        self.inner = ref_pipeline.synthetic_workload(cfg)
+        for lp in self.inner.layer_params:
+            for name in ("w_q", "w_k", "w_v", "w_out"):
+                setattr(lp, name, bf16_round(getattr(lp, name)))
+        self.layer_params = self.inner.layer_params
+
+    def x(self, t):
+        return bf16_round(self.inner.x(t))
+
+
+def pipeline_run():
+    """Reference run(): per-step last-layer outputs, step costs, final symbols."""
+    d = {}
+    for ci, kw in enumerate(RUN_CASES):
+        cfg = ref_pipeline.EngineConfig(b_q=T, b_k=T, d=T, **kw)
+        wl = _Bf16Workload(cfg)
+        res = ref_pipeline.run(cfg, wl)
+        p = f"r{ci}_"
+        # unrounded generator draws, to pin SyntheticWorkload's RNG sequence
+        raw = ref_pipeline.synthetic_workload(cfg)
+        lp = raw.layer_params[-1]
+        d[p + "w_probe"] = np.concatenate([lp.w_q[-1, -3:, :5].ravel(), lp.q_norm[0, :5],
+                                           lp.k_norm[-1, -5:], lp.w_out[0, :3, -5:].ravel()])
+        d[p + "x_probe"] = np.stack([raw.x(t)[-4:, :6] for t in range(cfg.steps)])
+        d[p + "out"] = np.stack(res.outputs).astype(np.float16)
+        d[p + "costs"] = np.array([[getattr(sc, k) for k in STEP_KEYS] for sc in res.step_costs],
+                                  np.int64)
+        d[p + "phase"] = np.array([sc.phase == "update" for sc in res.step_costs])
+        for li, st in enumerate(res.states):
+            d[p + f"l{li}_sc"] = np.stack([np.frombuffer(s.s_c, np.uint8) for s in st.symbols])
+            d[p + f"l{li}_ss"] = np.stack([np.frombuffer(s.s_s, np.uint8) for s in st.symbols])
+        r = res.report
+        d[p + "report"] = np.array([r.attn_pairs_total, r.attn_pairs_skipped, r.gemm_q_macs_dense,
+                                    r.gemm_q_macs_actual, r.gemm_o_macs_dense,
+                                    r.gemm_o_macs_actual, r.gemm_o_bias_macs], np.int64)
+        d[p + "speedups"] = np.array([r.sparsity, r.speedup_attention or 0.0, r.speedup_gemm_o])
+    d["n_cases"] = np.array(len(RUN_CASES))
+    np.savez_compressed(OUT / "run.npz", **d)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
+    if sys.argv[1:] == ["run"]:
+        pipeline_run()
+        sys.exit(0)
+    pipeline_run()
     policy()
     codec()
     attention()

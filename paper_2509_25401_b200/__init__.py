@@ -58,6 +58,25 @@ from .pipeline import (
     shard_heads,
     update_step,
 )
+from .costs import (
+    CostReport,
+    StepCost,
+    account_run,
+    sparsity,
+    theoretical_speedup_attention,
+    theoretical_speedup_gemm_o,
+)
+from .engine import (
+    Engine,
+    EngineConfig,
+    RunResult,
+    SyntheticWorkload,
+    config_from_dict,
+    dense_reference,
+    max_rel_error,
+    run,
+    synthetic_workload,
+)
 from .policy import MaskPolicy, generate_masks, generate_masks_heads, ramp_threshold
 from ._kernels import available_backends, get_backend
 

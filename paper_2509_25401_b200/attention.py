@@ -172,7 +172,7 @@ def _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, orde
 
 def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d, *, b_q=TILE,
                      b_k=TILE, mode="materialize", counters=None, backend=None, fill=0.0, out=None,
-                     stream=None, status=None, check=True):
+                     stream=None, status=None, check=True, plan=None, pairs=None):
     """Symbol-guided attention for every head of a layer (attention.py:150-221).
 
     q, k, v: bf16 [seq, heads, 128] on the GPU. symbols: DeviceSymbols.
@@ -180,7 +180,9 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     `out` (pre-filled with `fill` when `out` is not given); mode="materialize"
     writes their forecast. Returns out [seq, heads, 128] bf16.
     check=False defers the device contract checks (errors stay latched in the
-    status word) so the call never synchronises.
+    status word) so the call never synchronises. plan overrides the cached
+    schedule (the engine's static plans); pairs is an optional int64 [heads]
+    device accumulator of computed pairs (no host read).
     """
     if backend is not None and getattr(backend, "NAME", "b200") != "b200":
         raise ParameterError("this engine runs only its sm_100a kernels")
@@ -214,12 +216,14 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     else:
         # no cache at all: any cached block is a cold-cache StateError
         valid, vver = _zeros_valid(heads, t_q, q.device), -1
-    plan = symbols.plan(valid=valid, valid_version=vver, order_d=order_d, status=st,
-                        stream=stream, check=check)
+    if plan is None:
+        plan = symbols.plan(valid=valid, valid_version=vver, order_d=order_d, status=st,
+                            stream=stream, check=check)
     if out is None:
         out = torch.full((seq, heads, TILE), float(fill) if fill is not None else 0.0,
                          dtype=torch.bfloat16, device=q.device)
-    pairs = torch.zeros(heads, dtype=torch.int64, device=q.device) if counters is not None else None
+    if pairs is None and counters is not None:
+        pairs = torch.zeros(heads, dtype=torch.int64, device=q.device)
     _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads, TILE,
               symbols.s_s.data_ptr(), symbols.rows, symbols.cols, symbols.pool_n, plan.ptr(),
               1.0 / math.sqrt(TILE), 0, out.data_ptr(), None, None, order_d, _lib.ptr(pairs),

@@ -102,7 +102,8 @@ def _norm(norm_weight, heads):
 # GEMM-Q
 # ---------------------------------------------------------------------------
 def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, eps=1e-6,
-              counters=None, fill=0.0, out=None, rope=True, stream=None, status=None, check=True):
+              counters=None, fill=0.0, out=None, rope=True, stream=None, status=None, check=True,
+              plan=None):
     """Per-head query projection -> RMS norm -> rotary encoding (gemm.py:44-93).
 
     Update phase projects every tile; dispatch phase only the (block, head)
@@ -129,11 +130,13 @@ def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, 
     if out is None:
         out = torch.full((n, heads, TILE), 0.0 if fill is None else float(fill),
                          dtype=torch.bfloat16, device=x.device)
-    plan = None
     if phase == "dispatch":
         if symbols is None or symbols.heads != heads or symbols.rows != t_q:
             raise ShapeError(f"symbols must cover {heads} heads x {t_q} blocks")
-        plan = symbols.plan(status=status, stream=stream, check=check)
+        if plan is None:
+            plan = symbols.plan(status=status, stream=stream, check=check)
+    else:
+        plan = None
     _lib.call("fo_gemm_q", x.data_ptr(), n, dm, w.t.data_ptr(), heads, TILE, _lib.ptr(nw),
               _lib.ptr(cs), _lib.ptr(sn), float(eps), None if plan is None else plan.ptr(),
               1 if phase == "update" else 0, out.data_ptr(), stream_ptr(stream))
@@ -174,7 +177,7 @@ class CachedBias:
 
 
 def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE, counters=None,
-                       out=None, bias=None, stream=None, status=None, check=True):
+                       out=None, bias=None, stream=None, status=None, check=True, plan=None):
     """Update-step output projection, two stages in one pass (gemm.py:110-175).
     Returns (out bf16 [seq, d_model], CachedBias)."""
     require_cuda()
@@ -196,8 +199,9 @@ def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE
     if symbols_next.heads != heads or symbols_next.rows != t_q:
         raise ShapeError(f"symbols must cover {heads} heads x {t_q} blocks")
     st = status or Status.default()
-    plan = symbols_next.plan(valid=cache.valid, valid_version=cache.version, order_d=order_d,
-                             status=st, stream=stream, check=check)
+    if plan is None:
+        plan = symbols_next.plan(valid=cache.valid, valid_version=cache.version, order_d=order_d,
+                                 status=st, stream=stream, check=check)
     if out is None:
         out = torch.empty(n, dm, dtype=torch.bfloat16, device=o.device)
     stacks = bias.stacks if bias is not None else torch.empty(order_d + 1, n, dm,
@@ -206,7 +210,11 @@ def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE
     _lib.call("fo_gemm_o_update", o.data_ptr(), cache.stacks.data_ptr(), w.t.data_ptr(), n, heads,
               TILE, dm, order_d, plan.ptr(), out.data_ptr(), stacks.data_ptr(), st.ptr(),
               stream_ptr(stream))
-    orders = plan.orders_tensor().clone()
+    if bias is not None:
+        bias.orders.copy_(plan.orders_tensor())
+        orders = bias.orders
+    else:
+        orders = plan.orders_tensor().clone()
     if check:
         st.check("project_out_update")
     if counters is not None:
@@ -223,7 +231,7 @@ def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE
 
 
 def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, order_d, *, b_q=TILE,
-                         counters=None, out=None, stream=None, status=None, check=True):
+                         counters=None, out=None, stream=None, status=None, check=True, plan=None):
     """Dispatch-step output projection (gemm.py:178-229): active heads plus the
     forecast of the cached-head bias stacks."""
     require_cuda()
@@ -246,7 +254,8 @@ def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, o
                   heads, t_q, symbols.pool_n, st.ptr(), stream_ptr(stream))
         if check:
             st.check("project_out_dispatch")
-    plan = symbols.plan(status=st, stream=stream, check=check)
+    if plan is None:
+        plan = symbols.plan(status=st, stream=stream, check=check)
     coef = ctypes_floats(forecast_coefficients(elapsed_k, interval_n, order_d + 1))
     if out is None:
         out = torch.empty(n, dm, dtype=torch.bfloat16, device=o.device)

@@ -27,9 +27,15 @@ class Plan:
         self.offsets = [int(o) for o in offs]
 
     @classmethod
-    def build(cls, sym, valid=None, order_d=0, dense=False, status=None, stream=None, check=True):
+    def build(cls, sym, valid=None, order_d=0, dense=False, status=None, stream=None, check=True,
+              ws=None):
+        """ws: optional preallocated workspace, rewritten in place (the engine's
+        static per-layer plans, so captured CUDA graphs keep valid pointers)."""
         nbytes = _lib.load().fo_plan_workspace_bytes(sym.heads, sym.rows)
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=sym.s_c.device)
+        if ws is None:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=sym.s_c.device)
+        elif ws.numel() < nbytes or ws.dtype != torch.uint8:
+            raise ValueError(f"plan workspace needs {nbytes} uint8 bytes")
         st = status or Status.default()
         _lib.call("fo_plan", sym.s_c.data_ptr(), sym.s_s.data_ptr(), sym.heads, sym.rows, sym.cols,
                   sym.pool_n, int(bool(dense)), _lib.ptr(valid), int(order_d), ws.data_ptr(),

@@ -181,7 +181,7 @@ class DeviceSymbols:
 # ---------------------------------------------------------------------------
 # encoders (K1 on device)
 # ---------------------------------------------------------------------------
-def encode_symbols(cache_bits, skip_bits, pool_n, status=None, stream=None, check=True):
+def encode_symbols(cache_bits, skip_bits, pool_n, status=None, stream=None, check=True, out=None):
     """Pack every head at once. cache_bits [H, rows], skip_bits [H, rows, cols]
     (bool/uint8, any device) -> DeviceSymbols. Mirrors build_symbols
     (symbols.py:145-160) including its ConsistencyError for mixed pool groups."""
@@ -202,14 +202,22 @@ def encode_symbols(cache_bits, skip_bits, pool_n, status=None, stream=None, chec
         raise ShapeError(f"skip mask has {sb.shape[1]} rows, cache mask has {rows}")
     cols = sb.shape[2]
     comp_rows, comp_cols = ceil_div(rows, pool_n), ceil_div(cols, pool_n)
-    s_c = torch.empty(heads, ceil_div(comp_rows, 8), dtype=torch.uint8, device=cb.device)
-    s_s = torch.empty(heads, comp_rows, ceil_div(comp_cols, 8), dtype=torch.uint8, device=cb.device)
+    if out is not None:
+        # rewrite a resident DeviceSymbols in place (static buffers of the engine)
+        if (out.heads, out.rows, out.cols, out.pool_n) != (heads, rows, cols, pool_n):
+            raise ShapeError("encode_symbols: out geometry differs from the masks")
+        s_c, s_s = out.s_c, out.s_s
+        out.invalidate()
+    else:
+        s_c = torch.empty(heads, ceil_div(comp_rows, 8), dtype=torch.uint8, device=cb.device)
+        s_s = torch.empty(heads, comp_rows, ceil_div(comp_cols, 8), dtype=torch.uint8,
+                          device=cb.device)
     st = status or Status.default()
     _lib.call("fo_encode_symbols", cb.data_ptr(), sb.data_ptr(), heads, rows, cols, pool_n,
               s_c.data_ptr(), s_s.data_ptr(), st.ptr(), stream_ptr(stream))
     if check:
         st.check("encode_symbols")
-    return DeviceSymbols(s_c, s_s, rows, cols, pool_n)
+    return out if out is not None else DeviceSymbols(s_c, s_s, rows, cols, pool_n)
 
 
 def _bits(bits, ndim, name):
