@@ -99,6 +99,19 @@ FO_API int fo_sparse_attention(const void* q, const void* k, const void* v, int 
                         int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
                         void* stream);
 
+/* K2 in mode="materialize" as ONE launch (attention.py:150-221 with 212-216): the
+ * computed tiles as fo_sparse_attention, and the cached tiles' OP_reuse
+ * out = sum_{d < min(order_d+1, valid)} coef[d] * cache[d] fused into the same
+ * persistent kernel (its softmax warps take cached tiles from a global cursor
+ * once their attention items are done). cache [order_d+1, S, H*128] and valid
+ * are read-only here; coef is a host array of order_d+1 floats. The plan must
+ * be built with `valid` (cold-cache check). */
+FO_API int fo_sparse_attention_reuse(const void* q, const void* k, const void* v, int seq, int heads,
+                              int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                              const void* plan_ws, float scale, const void* cache,
+                              const int32_t* valid, int order_d, const float* coef, void* out,
+                              int64_t* pairs, uint32_t* status, void* stream);
+
 /* OP_reuse for mode="materialize": cached tiles of `out` <- sum_d coef[d]*stack[d]
  * (attention.py:96-113,212-216). coef is a host array of order_d+1 floats. */
 FO_API int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim, int rows,

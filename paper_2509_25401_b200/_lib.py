@@ -37,6 +37,8 @@ SIGNATURES = {
     "fo_plan": [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P],
     "fo_sparse_attention": [_P, _P, _P, _I, _I, _I, _P, _I, _I, _I, _P, _F, _I, _P, _P, _P, _I,
                             _P, _P, _P],
+    "fo_sparse_attention_reuse": [_P, _P, _P, _I, _I, _I, _P, _I, _I, _I, _P, _F, _P, _P, _I, _P,
+                                  _P, _P, _P, _P],
     "fo_forecast_materialize": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "fo_cache_push": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
     "fo_gemm_q": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _F, _P, _I, _P, _P],
@@ -58,7 +60,8 @@ _lib = None
 
 # entry point -> kernels it launches (gpu_launches accounting)
 LAUNCHING = {n: 1 for n in ("fo_encode_symbols", "fo_decode_symbols", "fo_plan",
-                            "fo_sparse_attention", "fo_forecast_materialize", "fo_cache_push",
+                            "fo_sparse_attention", "fo_sparse_attention_reuse",
+                            "fo_forecast_materialize", "fo_cache_push",
                             "fo_gemm_q", "fo_gemm_o_update", "fo_gemm_o_dispatch",
                             "fo_check_active_match")}
 LAUNCHING["fo_generate_masks"] = 5  # pool q, pool k, scores, cache select, skip select

@@ -224,17 +224,21 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
                          dtype=torch.bfloat16, device=q.device)
     if pairs is None and counters is not None:
         pairs = torch.zeros(heads, dtype=torch.int64, device=q.device)
-    _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads, TILE,
-              symbols.s_s.data_ptr(), symbols.rows, symbols.cols, symbols.pool_n, plan.ptr(),
-              1.0 / math.sqrt(TILE), 0, out.data_ptr(), None, None, order_d, _lib.ptr(pairs),
-              st.ptr(), stream_ptr(stream))
-    if mode == "materialize":
-        n_orders = order_d + 1
-        coef = ctypes_floats(forecast_coefficients(elapsed_k, interval_n, n_orders))
-        _lib.call("fo_forecast_materialize", cache.stacks.data_ptr(), seq, heads, TILE, t_q,
-                  order_d, plan.ptr(), cache.valid.data_ptr(), ctypes.addressof(coef),
-                  out.data_ptr(),
-                  stream_ptr(stream))
+    if mode == "materialize" and cache is not None and cache.stacks is not None:
+        # one launch: computed tiles + the cached tiles' OP_reuse fused in (K2r)
+        coef = ctypes_floats(forecast_coefficients(elapsed_k, interval_n, order_d + 1))
+        _lib.call("fo_sparse_attention_reuse", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq,
+                  heads, TILE, symbols.s_s.data_ptr(), symbols.rows, symbols.cols, symbols.pool_n,
+                  plan.ptr(), 1.0 / math.sqrt(TILE), cache.stacks.data_ptr(),
+                  cache.valid.data_ptr(), min(order_d, cache.order), ctypes.addressof(coef),
+                  out.data_ptr(), _lib.ptr(pairs), st.ptr(), stream_ptr(stream))
+    else:
+        # mode="bias" (cached rows untouched), or nothing cached can be read: the
+        # plan has latched a cold-cache StateError for any cached tile
+        _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads,
+                  TILE, symbols.s_s.data_ptr(), symbols.rows, symbols.cols, symbols.pool_n,
+                  plan.ptr(), 1.0 / math.sqrt(TILE), 0, out.data_ptr(), None, None, order_d,
+                  _lib.ptr(pairs), st.ptr(), stream_ptr(stream))
     if check:
         st.check("sparse_attention")
     if counters is not None:

@@ -57,6 +57,7 @@ struct Bars {
   uint64_t s_full[2];
   uint64_t p_full, o_done, o_last, o_free;
   uint32_t tmem_base;
+  int fc_tile;  // fused forecast: the tile the softmax warps take next
 };
 constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
 }  // namespace attn
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(attn::NTHREADS, 1)
     if (tim)
       for (int q = 0; q < 16; ++q) p.dbg[blockIdx.x * 32 + q] = tacc[q];
 #endif
+    if (p.fc_cache) forecast_cached_tiles<128>(p, threadIdx.x - 128, 8, &bars->fc_tile);
   }
   tc_fence_before();
   __syncthreads();

@@ -51,6 +51,7 @@ struct Bars {
   uint32_t tmem_base;
   float xmax[2][2][128];  // [tile parity][column half][row]: half-row maxima
   float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
+  int fc_tile;            // fused forecast: the tile the softmax warps take next
 };
 constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES <= 232448, "column-split attention exceeds shared memory");
@@ -472,6 +473,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
       }
     }
+    if (p.fc_cache)
+      forecast_cached_tiles<SOFTMAX_THREADS>(p, threadIdx.x - 128, 8, &bars->fc_tile);
   }
   tc_fence_before();
   __syncthreads();

@@ -184,11 +184,12 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
   return check_launch("plan");
 }
 
-int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, int heads,
-                        int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
-                        const void* plan_ws, float scale, int update_mode, void* out, void* cache,
-                        int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
-                        void* stream) {
+static int attention_common(const void* q, const void* k, const void* v, int seq, int heads,
+                            int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                            const void* plan_ws, float scale, int update_mode, void* out,
+                            void* cache, int32_t* valid, int order_d, int64_t* pairs,
+                            uint32_t* status, const void* fc_cache, const int32_t* fc_valid,
+                            const float* fc_coef, void* stream) {
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   rc = check_symbol_dims(heads, rows, cols, pool_n);
@@ -226,6 +227,11 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
   p.pairs = reinterpret_cast<long long*>(pairs);
   p.status = status;
   p.dbg = nullptr;
+  p.fc_cache = static_cast<const __nv_bfloat16*>(fc_cache);
+  p.fc_valid = fc_valid;
+  p.fc_counts = pv.counts;
+  p.fc_tiles = pv.gq_items;
+  for (int d = 0; d < 4; ++d) p.fc_coef[d] = (fc_coef && d <= order_d) ? fc_coef[d] : 0.f;
 #ifdef FO_ATTN_TIMING
   static long long* g_dbg = nullptr;
   if (!g_dbg) {
@@ -241,6 +247,28 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
   else
     launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
   return check_launch("sparse_attention");
+}
+
+int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, int heads,
+                        int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                        const void* plan_ws, float scale, int update_mode, void* out, void* cache,
+                        int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
+                        void* stream) {
+  return attention_common(q, k, v, seq, heads, head_dim, s_s, rows, cols, pool_n, plan_ws, scale,
+                          update_mode, out, cache, valid, order_d, pairs, status, nullptr, nullptr,
+                          nullptr, stream);
+}
+
+int fo_sparse_attention_reuse(const void* q, const void* k, const void* v, int seq, int heads,
+                              int head_dim, const uint8_t* s_s, int rows, int cols, int pool_n,
+                              const void* plan_ws, float scale, const void* cache,
+                              const int32_t* valid, int order_d, const float* coef, void* out,
+                              int64_t* pairs, uint32_t* status, void* stream) {
+  if (!cache || !valid || !coef)
+    return fail(FO_ERR_STATE, "materialize mode needs the feature cache, its valid orders and coef");
+  return attention_common(q, k, v, seq, heads, head_dim, s_s, rows, cols, pool_n, plan_ws, scale,
+                          0, out, nullptr, nullptr, order_d, pairs, status, cache, valid, coef,
+                          stream);
 }
 
 int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim, int rows,

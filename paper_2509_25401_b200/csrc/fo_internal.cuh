@@ -8,9 +8,11 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 
 // Per-layer schedule derived from the symbols (built by plan_kernel).
 struct PlanView {
-  int* counts;                // [0] attention items, [1] GEMM-Q tiles
+  int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
+                              // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting)
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
-  int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order
+  int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
+                              // the cached tiles in the same order from index counts[1]
   unsigned long long* hmask;  // [rows] bit h set = head h computed for block i
   int* orders;                // [rows] cached-bias orders per block (0 = no cached heads)
   long long* pairs_pred;      // [H] mask-predicted computed pairs
@@ -72,7 +74,83 @@ struct AttnParams {
   long long* pairs;       // [H] instrumented computed pairs, or null
   uint32_t* status;
   long long* dbg;         // FO_ATTN_TIMING builds: per-CTA phase cycle counters
+  // fused OP_reuse (mode="materialize"): once a CTA's attention items are done,
+  // its softmax warps forecast cached tiles into `out` (fc_cache null = off)
+  const __nv_bfloat16* fc_cache;  // [order+1, S, H*128] diff stacks
+  const int32_t* fc_valid;        // [H, t_q]
+  int* fc_counts;                 // plan counts: [1] active tiles, [2] cursor, [3] CTAs done
+  const int* fc_tiles;            // plan gq_items (cached tiles from index counts[1])
+  float fc_coef[4];
 };
+
+// OP_reuse for the cached tiles of one layer (attention.py:96-113,212-216):
+// out[tile] = sum_{d < min(order+1, valid)} coef[d] * stack[d][tile]. Run by
+// the NT softmax threads of every CTA after its attention items: tiles are
+// taken from a global cursor, so CTAs that finish their items early absorb
+// the forecast work. Each thread streams 2048/NT 16-byte chunks per tile with
+// all loads in flight. The last CTA out resets the cursor (graph replays).
+template <int NT>
+__device__ __forceinline__ void forecast_cached_tiles(const AttnParams& p, int s, int bar_id,
+                                                      int* sh_tile) {
+  constexpr int PER = 4;  // 16-byte chunks per thread in flight (x up to 4 orders)
+  const int n_cached = p.H * p.t_q - p.fc_counts[1];
+  const size_t HD = (size_t)p.H * kTile, SS = (size_t)p.S * HD;
+  for (;;) {
+    if (s == 0) *sh_tile = atomicAdd(&p.fc_counts[2], 1);
+    named_bar_sync(bar_id, NT);
+    const int k = *sh_tile;
+    named_bar_sync(bar_id, NT);
+    if (k >= n_cached) break;
+    const int code = p.fc_tiles[p.fc_counts[1] + k];
+    const int h = code >> 20, i = code & 0xFFFFF;
+    const int n = min(p.order_d + 1, p.fc_valid[(size_t)h * p.t_q + i]);
+    const int chunks = min(kTile, p.S - i * kTile) * 16;
+#pragma unroll 1
+    for (int e0 = s; e0 < chunks; e0 += PER * NT) {
+    uint4 w[PER][4];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = e0 + u * NT;
+      const size_t off = (size_t)(i * kTile + (e >> 4)) * HD + (size_t)h * kTile + (e & 15) * 8;
+#pragma unroll
+      for (int d = 0; d < 4; ++d)
+        if (e < chunks && d < n)
+          w[u][d] = __ldcs(reinterpret_cast<const uint4*>(p.fc_cache + d * SS + off));
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = e0 + u * NT;
+      if (e >= chunks) continue;
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        if (d >= n) break;
+        const uint32_t w4[4] = {w[u][d].x, w[u][d].y, w[u][d].z, w[u][d].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = fmaf(p.fc_coef[d], bf16lo(w4[q]), acc[2 * q]);
+          acc[2 * q + 1] = fmaf(p.fc_coef[d], bf16hi(w4[q]), acc[2 * q + 1]);
+        }
+      }
+      uint4 pk;
+      pk.x = pack_bf16x2(acc[0], acc[1]);
+      pk.y = pack_bf16x2(acc[2], acc[3]);
+      pk.z = pack_bf16x2(acc[4], acc[5]);
+      pk.w = pack_bf16x2(acc[6], acc[7]);
+      const size_t off = (size_t)(i * kTile + (e >> 4)) * HD + (size_t)h * kTile + (e & 15) * 8;
+      __stcs(reinterpret_cast<uint4*>(p.out + off), pk);
+    }
+    }
+  }
+  if (s == 0) {
+    __threadfence();
+    if (atomicAdd(&p.fc_counts[3], 1) == (int)gridDim.x - 1) {
+      p.fc_counts[2] = 0;
+      p.fc_counts[3] = 0;
+      __threadfence();
+    }
+  }
+}
 
 void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                       const AttnParams& p, int grid, cudaStream_t stream);

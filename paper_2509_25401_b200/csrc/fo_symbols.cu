@@ -229,12 +229,21 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     scan[tid] += v;
     __syncthreads();
   }
+  const int n_active = scan[nt - 1];
   int pos = scan[tid] - local;
+  int pos_c = n_active + (lo - pos);  // cached tiles follow the active ones, same order
   for (int idx = lo; idx < hi; ++idx) {
     int i = idx / H, h = idx % H;
-    if (is_active(h, i)) pv.gq_items[pos++] = (h << 20) | i;
+    if (is_active(h, i))
+      pv.gq_items[pos++] = (h << 20) | i;
+    else
+      pv.gq_items[pos_c++] = (h << 20) | i;
   }
-  if (tid == nt - 1) pv.counts[1] = scan[nt - 1];
+  if (tid == nt - 1) {
+    pv.counts[1] = n_active;
+    pv.counts[2] = 0;  // fused-forecast cursor and CTA count (attention, materialize mode)
+    pv.counts[3] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
