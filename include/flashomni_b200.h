@@ -59,9 +59,9 @@ FO_API const char* fo_last_error(void);
 FO_API int fo_num_sms(void);
 
 /* Schedule workspace for one layer's symbols (plan): byte size and the byte
- * offsets of {counts, items, gemm-q items, head masks, orders, pairs}. */
+ * offsets of {counts, items, gemm-q tiles, head masks, orders, pairs, gemm-q head-pair jobs}. */
 FO_API size_t fo_plan_workspace_bytes(int heads, int rows);
-FO_API void fo_plan_offsets(int heads, int rows, size_t offsets[6]);
+FO_API void fo_plan_offsets(int heads, int rows, size_t offsets[7]);
 
 /* K1 symbol pack. Replaces encode_cache_mask / encode_skip_mask / build_symbols
  * (reference pkg/src/omniattn/symbols.py:65-81,145-160) for all heads at once.

@@ -128,7 +128,7 @@ int fo_num_sms(void) { return num_sms(); }
 
 size_t fo_plan_workspace_bytes(int heads, int rows) { return plan_layout(heads, rows, nullptr, nullptr); }
 
-void fo_plan_offsets(int heads, int rows, size_t offsets[6]) {
+void fo_plan_offsets(int heads, int rows, size_t offsets[7]) {
   PlanView pv;
   plan_layout(heads, rows, nullptr, &pv);
   offsets[0] = reinterpret_cast<size_t>(pv.counts);
@@ -137,6 +137,7 @@ void fo_plan_offsets(int heads, int rows, size_t offsets[6]) {
   offsets[3] = reinterpret_cast<size_t>(pv.hmask);
   offsets[4] = reinterpret_cast<size_t>(pv.orders);
   offsets[5] = reinterpret_cast<size_t>(pv.pairs_pred);
+  offsets[6] = reinterpret_cast<size_t>(pv.gq_pairs);
 }
 
 int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int heads, int rows,
@@ -318,10 +319,10 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   p.dense = dense;
   if (plan_ws) {
     PlanView pv = plan_view(plan_ws, heads, t_q);
-    p.gq_items = pv.gq_items;
-    p.n_gq = pv.counts + 1;
+    p.gq_pairs = pv.gq_pairs;
+    p.n_gq = pv.counts + 4;
   } else {
-    p.gq_items = nullptr;
+    p.gq_pairs = nullptr;
     p.n_gq = nullptr;
   }
   p.norm_w = norm_w;

@@ -27,10 +27,13 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STAGES = 6;
 constexpr int NTHREADS = 256;
 
-// GEMM-O dispatch: one stage fewer, and a ring of bias / output chunks
-// (128 rows x 32 columns, orders 0 and 1, SW64) between the bias-loader warp,
-// the epilogue and the TMA store
-constexpr int D_STAGES = 5;
+// GEMM-O dispatch: 128 x 256 output tiles (N=256 halves the W/A feed per MMA
+// cycle relative to N=128 for A), 3 stages of 48 KB, and a ring of bias /
+// output chunks (128 rows x 32 columns, orders 0 and 1, SW64) between the
+// bias-loader warp, the epilogue and the TMA store
+constexpr int D_BN = 256;
+constexpr int D_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
+constexpr int D_STAGES = 3;
 constexpr int BIAS_SLOTS = 4;
 constexpr int BIAS_ORDER_BYTES = BM * 32 * 2;  // 8 KB
 constexpr int BIAS_SLOT_BYTES = 2 * BIAS_ORDER_BYTES;
@@ -43,7 +46,7 @@ struct Bars {
 };
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
 constexpr int SMEM_BYTES_D =
-    D_STAGES * STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES + 1024 + (int)sizeof(Bars);
+    D_STAGES * D_STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
 __device__ __forceinline__ void init_bars(Bars* b) {
@@ -106,6 +109,19 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 // =============================================================================
 // GEMM-Q
 // =============================================================================
+// Job = query block i x up to two heads (the plan pairs block i's active heads
+// in order): one 128 x 256 tcgen05 tile (128 x 128 for an odd head out). N=256
+// cuts the operand feed per MMA cycle from 128 to 96 B/SM (A is shared by the
+// two heads), which is what bounds a 128 x 128 mainloop. Each head's 128
+// accumulator columns get RMSNorm + RoPE in the epilogue.
+namespace gemm {
+constexpr int Q_BN = 256;
+constexpr int Q_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
+constexpr int Q_STAGES = 4;
+constexpr int Q_SMEM_BYTES = Q_STAGES * Q_STAGE_BYTES + 1024 + (int)sizeof(Bars);
+static_assert(Q_SMEM_BYTES <= 232448, "GEMM-Q shared memory over the sm_100 limit");
+}  // namespace gemm
+
 __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     gemm_q_kernel(const __grid_constant__ CUtensorMap xm, const __grid_constant__ CUtensorMap wm,
                   const GemmQParams p) {
@@ -113,44 +129,49 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  Bars* bars = reinterpret_cast<Bars*>(smem + STAGES * STAGE_BYTES);
+  Bars* bars = reinterpret_cast<Bars*>(smem + Q_STAGES * Q_STAGE_BYTES);
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     init_bars(bars);
     tma_prefetch_desc(&xm);
     tma_prefetch_desc(&wm);
   }
-  if (warp == 2) tmem_alloc<256>(&bars->tmem_base);
+  if (warp == 2) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
-  const int n_jobs = p.dense ? p.t_q * p.H : *p.n_gq;
+  const int nph = (p.H + 1) >> 1;  // head pairs per block (dense phase)
+  const int n_jobs = p.dense ? p.t_q * nph : *p.n_gq;
   const int nkb = p.dm / BK;
-  auto job = [&](int w, int& h, int& i) {
+  auto job = [&](int w, int& i, int& h1, int& h2) {
     if (p.dense) {
-      i = w / p.H;
-      h = w % p.H;
+      i = w / nph;
+      h1 = 2 * (w - i * nph);
+      h2 = (h1 + 1 < p.H) ? h1 + 1 : -1;
     } else {
-      const int it = p.gq_items[w];
-      h = it >> 20;
-      i = it & 0xFFFFF;
+      const int c = p.gq_pairs[w];
+      i = c & 0xFFFF;
+      h1 = (c >> 16) & 0xFF;
+      h2 = (c >> 24) - 1;
     }
   };
 
   if (warp == 0) {
     // TMA producer (whole warp walks the schedule; one elected lane issues)
-    Ring<> rg;
+    Ring<Q_STAGES> rg;
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
-      int h, i;
-      job(w, h, i);
+      int i, h1, h2;
+      job(w, i, h1, h2);
+      const uint32_t bytes = A_BYTES + (h2 >= 0 ? 2 : 1) * B_BYTES;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
-          uint8_t* st = smem + rg.s * STAGE_BYTES;
-          mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
+          uint8_t* st = smem + rg.s * Q_STAGE_BYTES;
+          mbar_arrive_expect_tx(&bars->full[rg.s], bytes);
           tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
-          tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h * BN);
+          tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h1 * BN);
+          if (h2 >= 0) tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], kb * BK, h2 * BN);
         }
         __syncwarp();
         rg.next();
@@ -158,19 +179,23 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     }
   } else if (warp == 1) {
     // MMA issuer (warp-uniform schedule, elected lane issues + commits)
-    const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+    const uint32_t idesc2 = make_idesc_bf16(BM, Q_BN, false, false);
+    const uint32_t idesc1 = make_idesc_bf16(BM, BN, false, false);
     const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
-    Ring<> rg;
+    Ring<Q_STAGES> rg;
     int t = 0;
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+      int i, h1, h2;
+      job(w, i, h1, h2);
+      const uint32_t idesc = h2 >= 0 ? idesc2 : idesc1;
       const int acc = t & 1;
       mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d = tbase + acc * BN;
+      const uint32_t d = tbase + acc * Q_BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->full[rg.s], rg.ph);
         tc_fence_after();
-        const uint64_t a = desc0 + (uint64_t)((rg.s * STAGE_BYTES) >> 4);
+        const uint64_t a = desc0 + (uint64_t)((rg.s * Q_STAGE_BYTES) >> 4);
         if (elect_one()) {
           mma_kblock(d, a, a + (A_BYTES >> 4), idesc, kb > 0);
           tc_commit(&bars->empty[rg.s]);
@@ -186,38 +211,48 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const size_t HD = (size_t)p.H * 128;
+    const bool rope = p.rope_cos != nullptr;
     int t = 0;
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
-      int h, i;
-      job(w, h, i);
+      int i, h1, h2;
+      job(w, i, h1, h2);
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      uint32_t u[4][32];
-      const uint32_t ta = tbase + lane_off + acc * BN;
-      tmem_ld32(ta + 0, u[0]);
-      tmem_ld32(ta + 32, u[1]);
-      tmem_ld32(ta + 64, u[2]);
-      tmem_ld32(ta + 96, u[3]);
-      tmem_ld_wait();
-      gemm::reg_fence(u[0]);
-      gemm::reg_fence(u[1]);
-      gemm::reg_fence(u[2]);
-      gemm::reg_fence(u[3]);
-      tc_fence_before();
-      mbar_arrive(&bars->tempty[acc]);
       const int row = i * BM + r;
-      __nv_bfloat16* dst = p.q + (size_t)row * HD + (size_t)h * 128;
-      if (row < p.S && !p.norm_w) {
-        // plain projection (V): no normalisation, no rotary encoding
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float o[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[c][k]);
-          gemm::store_bf16x32(dst + c * 32, o);
+      const int nh = h2 >= 0 ? 2 : 1;
+      const float* cs = rope ? p.rope_cos + (size_t)row * 64 : nullptr;
+      const float* sn = rope ? p.rope_sin + (size_t)row * 64 : nullptr;
+      for (int sl = 0; sl < nh; ++sl) {
+        const int h = sl ? h2 : h1;
+        uint32_t u[4][32];
+        const uint32_t ta = tbase + lane_off + acc * Q_BN + sl * BN;
+        tmem_ld32(ta + 0, u[0]);
+        tmem_ld32(ta + 32, u[1]);
+        tmem_ld32(ta + 64, u[2]);
+        tmem_ld32(ta + 96, u[3]);
+        tmem_ld_wait();
+        gemm::reg_fence(u[0]);
+        gemm::reg_fence(u[1]);
+        gemm::reg_fence(u[2]);
+        gemm::reg_fence(u[3]);
+        if (sl == nh - 1) {  // accumulator drained: release it to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&bars->tempty[acc]);
         }
-      } else if (row < p.S) {
+        if (row >= p.S) continue;
+        __nv_bfloat16* dst = p.q + (size_t)row * HD + (size_t)h * 128;
+        if (!p.norm_w) {
+          // plain projection (V): no normalisation, no rotary encoding
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float o[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[c][k]);
+            gemm::store_bf16x32(dst + c * 32, o);
+          }
+          continue;
+        }
         // RMSNorm (tensor.py:68-80): y * w / sqrt(mean(y^2) + eps)
         float ss = 0.f;
 #pragma unroll
@@ -229,26 +264,23 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           }
         const float inv = rsqrtf(ss * (1.f / 128.f) + p.eps);
         const float* nw = p.norm_w + (size_t)h * 128;
-        const bool rope = p.rope_cos != nullptr;
-        const float* cs = rope ? p.rope_cos + (size_t)row * 64 : nullptr;
-        const float* sn = rope ? p.rope_sin + (size_t)row * 64 : nullptr;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float o[32];
           // 16-byte vector loads of the norm weights and the rotary table
           float wv[32], cvv[16], svv[16];
 #pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 t4 = __ldg(reinterpret_cast<const float4*>(nw + c * 32) + q4);
-            wv[4 * q4] = t4.x; wv[4 * q4 + 1] = t4.y; wv[4 * q4 + 2] = t4.z; wv[4 * q4 + 3] = t4.w;
+          for (int q = 0; q < 8; ++q) {
+            const float4 t4 = __ldg(reinterpret_cast<const float4*>(nw + c * 32) + q);
+            wv[4 * q] = t4.x; wv[4 * q + 1] = t4.y; wv[4 * q + 2] = t4.z; wv[4 * q + 3] = t4.w;
           }
           if (rope) {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const float4 a4 = __ldg(reinterpret_cast<const float4*>(cs + c * 16) + q4);
-              const float4 b4 = __ldg(reinterpret_cast<const float4*>(sn + c * 16) + q4);
-              cvv[4 * q4] = a4.x; cvv[4 * q4 + 1] = a4.y; cvv[4 * q4 + 2] = a4.z; cvv[4 * q4 + 3] = a4.w;
-              svv[4 * q4] = b4.x; svv[4 * q4 + 1] = b4.y; svv[4 * q4 + 2] = b4.z; svv[4 * q4 + 3] = b4.w;
+            for (int q = 0; q < 4; ++q) {
+              const float4 a4 = __ldg(reinterpret_cast<const float4*>(cs + c * 16) + q);
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(sn + c * 16) + q);
+              cvv[4 * q] = a4.x; cvv[4 * q + 1] = a4.y; cvv[4 * q + 2] = a4.z; cvv[4 * q + 3] = a4.w;
+              svv[4 * q] = b4.x; svv[4 * q + 1] = b4.y; svv[4 * q + 2] = b4.z; svv[4 * q + 3] = b4.w;
             }
           }
 #pragma unroll
@@ -274,7 +306,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<256>(tbase);
+    tmem_dealloc<512>(tbase);
   }
 }
 
@@ -298,12 +330,14 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                   const GemmOParams p) {
   using namespace gemm;
   constexpr int ST = UPDATE ? STAGES : D_STAGES;
-  constexpr int ACC_COLS = UPDATE ? 2 * BN : BN;  // update: accumulator A (active) + B (cached)
-  constexpr int TM_COLS = UPDATE ? 512 : 256;
+  constexpr int SB = UPDATE ? STAGE_BYTES : D_STAGE_BYTES;  // bytes per stage
+  constexpr int TBN = UPDATE ? BN : D_BN;                     // output tile columns
+  constexpr int ACC_COLS = UPDATE ? 2 * BN : D_BN;  // update: accumulator A (active) + B (cached)
+  constexpr int TM_COLS = 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* ring = smem + ST * STAGE_BYTES;  // dispatch bias / output chunks
+  uint8_t* ring = smem + ST * SB;  // dispatch bias / output chunks
   Bars* bars = reinterpret_cast<Bars*>(ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES));
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
@@ -318,7 +352,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
-  const int nbn = p.dm / BN;
+  const int nbn = (p.dm + TBN - 1) / TBN;
+  // columns of n-tile nb (dispatch: the last tile is 128 wide when dm % 256 != 0)
+  auto tile_cols = [&](int nb) { return min(TBN, p.dm - nb * TBN); };
   const int nord = UPDATE ? p.order_d + 1 : 1;
   const int n_jobs = p.t_q * nbn * nord;
   const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
@@ -355,13 +391,17 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           while (m) {
             const int h = __ffsll(m) - 1;
             m &= m - 1;
+            const bool two = tile_cols(nb) > BN;
             for (int kk = 0; kk < 2; ++kk) {
               mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
               if (elect_one()) {
-                uint8_t* st = smem + rg.s * STAGE_BYTES;
-                mbar_arrive_expect_tx(&bars->full[rg.s], STAGE_BYTES);
+                uint8_t* st = smem + rg.s * SB;
+                mbar_arrive_expect_tx(&bars->full[rg.s], A_BYTES + (two ? 2 : 1) * B_BYTES);
                 tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
-                tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * BN);
+                tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * TBN);
+                if (two)
+                  tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
+                              nb * TBN + BN);
               }
               __syncwarp();
               rg.next();
@@ -373,13 +413,15 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     {
-      const uint32_t idesc = make_idesc_bf16(BM, BN, false, false);
+      const uint32_t idesc1 = make_idesc_bf16(BM, BN, false, false);
+      const uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, false);
       const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
       Ring<ST> rg;
       int t = 0;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
         int i, nb, d;
         if (!job(w, i, nb, d)) continue;
+        const uint32_t idesc = tile_cols(nb) > BN ? idesc2 : idesc1;
         const int acc = t & 1;
         mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -395,7 +437,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&bars->full[rg.s], rg.ph);
             tc_fence_after();
-            const uint64_t a = desc0 + (uint64_t)((rg.s * STAGE_BYTES) >> 4);
+            const uint64_t a = desc0 + (uint64_t)((rg.s * SB) >> 4);
             if (elect_one()) {
               mma_kblock(dst, a, a + (A_BYTES >> 4), idesc, kb > 0);
               tc_commit(&bars->empty[rg.s]);
@@ -416,21 +458,23 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
       const int nb = w % nbn, i = w / nbn;
       const int ns = staged_orders(i);
+      const int nch = tile_cols(nb) / 32;
       const int wn = w + gridDim.x;
       if (wn < n_jobs && elect_one()) {
         const int nb2 = wn % nbn, i2 = wn / nbn;
         const int ns2 = staged_orders(i2);
         for (int dd = 0; dd < ns2; ++dd)
-          for (int c = 0; c < 4; ++c) tma_prefetch_l2_2d(&cm, nb2 * BN + c * 32, dd * p.S + i2 * BM);
+          for (int c = 0; c < tile_cols(nb2) / 32; ++c)
+            tma_prefetch_l2_2d(&cm, nb2 * TBN + c * 32, dd * p.S + i2 * BM);
       }
       __syncwarp();
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < nch; ++c) {
         mbar_wait(&bars->bempty[rb.s], rb.ph ^ 1);
         if (elect_one()) {
           uint8_t* slot = ring + rb.s * BIAS_SLOT_BYTES;
           mbar_arrive_expect_tx(&bars->bfull[rb.s], ns * BIAS_ORDER_BYTES);
           for (int dd = 0; dd < ns; ++dd)
-            tma_load_2d(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s], nb * BN + c * 32,
+            tma_load_2d(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s], nb * TBN + c * 32,
                         dd * p.S + i * BM);
         }
         __syncwarp();
@@ -494,6 +538,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       int t = 0;
       for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
         const int nb = w % nbn, i = w / nbn;
+        const int nch = tile_cols(nb) / 32;
         const int acc = t & 1;
         const bool hasA = p.hmask[i] != 0ull;
         const int no = min(p.order_d + 1, p.orders[i]);
@@ -503,7 +548,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
         mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tA = tbase + lane_off + acc * ACC_COLS;
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < nch; ++c) {
           uint32_t ua[32];
           if (hasA) {
             tmem_ld32(tA + c * 32, ua);
@@ -512,7 +557,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
 #pragma unroll
             for (int k = 0; k < 32; ++k) ua[k] = 0u;
           }
-          if (c == 3) {  // accumulator drained: release it to the MMA warp
+          if (c == nch - 1) {  // accumulator drained: release it to the MMA warp
             tc_fence_before();
             mbar_arrive(&bars->tempty[acc]);
           }
@@ -546,7 +591,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
               if (!row_ok) break;
               const float cf = dd == 2 ? c2 : c3;
               const uint4 b = __ldg(reinterpret_cast<const uint4*>(
-                  p.bias + dd * SD + (size_t)row * p.dm + (size_t)nb * BN + c * 32 + q * 8));
+                  p.bias + dd * SD + (size_t)row * p.dm + (size_t)nb * TBN + c * 32 + q * 8));
               const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -561,7 +606,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           named_bar_sync(1, 128);
           if (warp == 4) {
             if (elect_one()) {
-              tma_store_2d(&om, ring + rb.s * BIAS_SLOT_BYTES, nb * BN + c * 32, i * BM);
+              tma_store_2d(&om, ring + rb.s * BIAS_SLOT_BYTES, nb * TBN + c * 32, i * BM);
               bulk_commit();
               bulk_wait_read<1>();  // the previous chunk's store has read its slot
               if (prev >= 0) mbar_arrive(&bars->bempty[prev]);
@@ -592,10 +637,10 @@ void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQPara
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(gemm_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm::SMEM_BYTES);
+                         gemm::Q_SMEM_BYTES);
     configured = true;
   }
-  gemm_q_kernel<<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(xm, wm, p);
+  gemm_q_kernel<<<grid, gemm::NTHREADS, gemm::Q_SMEM_BYTES, stream>>>(xm, wm, p);
 }
 
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,

@@ -9,14 +9,21 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 // Per-layer schedule derived from the symbols (built by plan_kernel).
 struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
-                              // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting)
+                              // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
+                              // [4] GEMM-Q head-pair jobs
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
   int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
                               // the cached tiles in the same order from index counts[1]
   unsigned long long* hmask;  // [rows] bit h set = head h computed for block i
   int* orders;                // [rows] cached-bias orders per block (0 = no cached heads)
   long long* pairs_pred;      // [H] mask-predicted computed pairs
+  int* gq_pairs;              // [H*rows] GEMM-Q jobs: block i x up to two active heads,
+                              // i | h1 << 16 | (h2 + 1) << 24 (h2 = -1: single head)
 };
+
+__host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
+  return i | (h1 << 16) | ((h2 + 1) << 24);
+}
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -27,12 +34,13 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     off = align16(off + bytes);
     return o;
   };
-  size_t o_counts = take(4 * sizeof(int));
+  size_t o_counts = take(8 * sizeof(int));
   size_t o_items = take((size_t)H * rows * sizeof(int2));
   size_t o_gq = take((size_t)H * rows * sizeof(int));
   size_t o_hm = take((size_t)rows * sizeof(unsigned long long));
   size_t o_ord = take((size_t)rows * sizeof(int));
   size_t o_pairs = take((size_t)H * sizeof(long long));
+  size_t o_gqp = take((size_t)H * rows * sizeof(int));
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -40,6 +48,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->hmask = reinterpret_cast<unsigned long long*>(base + o_hm);
     pv->orders = reinterpret_cast<int*>(base + o_ord);
     pv->pairs_pred = reinterpret_cast<long long*>(base + o_pairs);
+    pv->gq_pairs = reinterpret_cast<int*>(base + o_gqp);
   }
   return off;
 }
@@ -163,8 +172,8 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
 // ---------------------------------------------------------------------------
 struct GemmQParams {
   int S, dm, H, t_q, dense;
-  const int* gq_items;
-  const int* n_gq;
+  const int* gq_pairs;  // plan head-pair jobs (sparse phase)
+  const int* n_gq;      // their count
   const float* norm_w;  // [H, 128]
   const float* rope_cos;  // [S, 64]
   const float* rope_sin;  // [S, 64]

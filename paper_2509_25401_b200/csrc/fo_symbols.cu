@@ -244,6 +244,37 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     pv.counts[2] = 0;  // fused-forecast cursor and CTA count (attention, materialize mode)
     pv.counts[3] = 0;
   }
+  // pass 4: GEMM-Q head-pair jobs. Block i's active heads are paired in order
+  // (an odd one out runs alone), so every job is one N=256 (or N=128) tile and
+  // no skipped tile is ever computed. Jobs are block-major.
+  __syncthreads();  // pass 3 read scan[]; hmask (pass 1) is visible block-wide
+  const int per_b = ceil_div_d(rows, nt);
+  const int blo = min(rows, tid * per_b), bhi = min(rows, blo + per_b);
+  int nloc = 0;
+  for (int i = blo; i < bhi; ++i) nloc += (__popcll(pv.hmask[i]) + 1) >> 1;
+  scan[tid] = nloc;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    int v = tid >= off ? scan[tid - off] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int jp = scan[tid] - nloc;
+  for (int i = blo; i < bhi; ++i) {
+    unsigned long long m = pv.hmask[i];
+    while (m) {
+      const int h1 = __ffsll(m) - 1;
+      m &= m - 1;
+      int h2 = -1;
+      if (m) {
+        h2 = __ffsll(m) - 1;
+        m &= m - 1;
+      }
+      pv.gq_pairs[jp++] = gq_pair_code(i, h1, h2);
+    }
+  }
+  if (tid == nt - 1) pv.counts[4] = scan[nt - 1];
 }
 
 // ---------------------------------------------------------------------------

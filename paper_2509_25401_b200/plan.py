@@ -22,7 +22,7 @@ class Plan:
     def __init__(self, ws, heads, rows, dense):
         self.ws = ws
         self.heads, self.rows, self.dense = heads, rows, dense
-        offs = (ctypes.c_size_t * 6)()
+        offs = (ctypes.c_size_t * 7)()
         _lib.load().fo_plan_offsets(heads, rows, offs)
         self.offsets = [int(o) for o in offs]
 
@@ -53,7 +53,7 @@ class Plan:
 
     # host-side inspection (synchronising; used by counters and tests)
     def counts(self):
-        return self._view(0, torch.int32, 4).cpu().numpy()
+        return self._view(0, torch.int32, 8).cpu().numpy()
 
     def items(self):
         n = int(self.counts()[0])
@@ -73,3 +73,9 @@ class Plan:
 
     def pairs_pred(self):
         return self._view(5, torch.int64, self.heads).cpu().numpy()
+
+    def gq_pairs(self):
+        """GEMM-Q jobs: (block, head1, head2 or -1), one N=256 (or 128) tile each."""
+        n = int(self._view(0, torch.int32, 8)[4].item())
+        it = self._view(6, torch.int32, self.heads * self.rows)[:n].cpu().numpy()
+        return np.stack([it & 0xFFFF, (it >> 16) & 0xFF, (it >> 24) - 1], axis=1)
