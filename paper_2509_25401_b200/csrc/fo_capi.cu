@@ -308,7 +308,8 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64]");
   if (!dense && !plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
   CUtensorMap xm, wm;
-  if ((rc = make_map(&xm, x, seq, d_model, 128, "x"))) return rc;
+  // x moves in half tiles (64 rows), each multicast to both CTAs of a cluster
+  if ((rc = make_map(&xm, x, seq, d_model, 64, "x"))) return rc;
   if ((rc = make_map(&wm, w_qt, (uint64_t)heads * kTile, d_model, 128, "w_q"))) return rc;
   const int t_q = ceil_div_d(seq, kTile);
   GemmQParams p;
@@ -320,17 +321,19 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   if (plan_ws) {
     PlanView pv = plan_view(plan_ws, heads, t_q);
     p.gq_pairs = pv.gq_pairs;
-    p.n_gq = pv.counts + 4;
+    p.gq_cjobs = pv.gq_cjobs;
+    p.n_gqc = pv.counts + 5;
   } else {
     p.gq_pairs = nullptr;
-    p.n_gq = nullptr;
+    p.gq_cjobs = nullptr;
+    p.n_gqc = nullptr;
   }
   p.norm_w = norm_w;
   p.rope_cos = rope_cos;
   p.rope_sin = rope_sin;
   p.eps = eps;
   p.q = static_cast<__nv_bfloat16*>(q_out);
-  launch_gemm_q(xm, wm, p, num_sms(), (cudaStream_t)stream);
+  launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
   return check_launch("gemm_q");
 }
 

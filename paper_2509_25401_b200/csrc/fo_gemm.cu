@@ -16,6 +16,8 @@
 // Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..7 epilogue
 // (one accumulator row per thread). TMEM accumulators are double-buffered so
 // the epilogue of tile t overlaps the mainloop of tile t+1.
+#include <algorithm>
+
 #include "fo_internal.cuh"
 
 namespace fo {
@@ -49,10 +51,12 @@ constexpr int SMEM_BYTES_D =
     D_STAGES * D_STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
-__device__ __forceinline__ void init_bars(Bars* b) {
+// empty_count: consumers that release a stage (2 when the A tile is multicast
+// across a CTA pair: both MMA warps must be done before either producer refills)
+__device__ __forceinline__ void init_bars(Bars* b, uint32_t empty_count = 1) {
   for (int s = 0; s < STAGES; ++s) {
     mbar_init(&b->full[s], 1);
-    mbar_init(&b->empty[s], 1);
+    mbar_init(&b->empty[s], empty_count);
   }
   for (int a = 0; a < 2; ++a) {
     mbar_init(&b->tfull[a], 1);
@@ -112,70 +116,99 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 // Job = query block i x up to two heads (the plan pairs block i's active heads
 // in order): one 128 x 256 tcgen05 tile (128 x 128 for an odd head out). N=256
 // cuts the operand feed per MMA cycle from 128 to 96 B/SM (A is shared by the
-// two heads), which is what bounds a 128 x 128 mainloop. Each head's 128
-// accumulator columns get RMSNorm + RoPE in the epilogue.
+// two heads). CTAs run in 2-CTA clusters that take two jobs of the same block:
+// each CTA loads half of the x tile and multicasts it to both, cutting the
+// L2 -> SM feed to 80 B per MMA cycle (the mainloop is feed-bound: ncu shows
+// the producer waiting on free stages while the MMA warp waits on data). Each
+// head's 128 accumulator columns get RMSNorm + RoPE in the epilogue.
 namespace gemm {
 constexpr int Q_BN = 256;
 constexpr int Q_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
 constexpr int Q_STAGES = 4;
-constexpr int Q_SMEM_BYTES = Q_STAGES * Q_STAGE_BYTES + 1024 + (int)sizeof(Bars);
+constexpr int Q_NW_BYTES = 64 * 128 * 4;  // RMSNorm weights of up to 64 heads
+constexpr int Q_SMEM_BYTES = Q_STAGES * Q_STAGE_BYTES + 1024 + 1024 + Q_NW_BYTES;
+constexpr int A_HALF_BYTES = A_BYTES / 2;  // 64 rows x 64 K, SW128
 static_assert(Q_SMEM_BYTES <= 232448, "GEMM-Q shared memory over the sm_100 limit");
 }  // namespace gemm
 
 __global__ void __launch_bounds__(gemm::NTHREADS, 1)
-    gemm_q_kernel(const __grid_constant__ CUtensorMap xm, const __grid_constant__ CUtensorMap wm,
-                  const GemmQParams p) {
+    gemm_q_kernel(const __grid_constant__ CUtensorMap xm,  // x, box 64 K x 64 rows (half tile)
+                  const __grid_constant__ CUtensorMap wm, const GemmQParams p) {
   using namespace gemm;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + Q_STAGES * Q_STAGE_BYTES);
+  float* nw_smem = reinterpret_cast<float*>(smem + Q_STAGES * Q_STAGE_BYTES + 1024);
   const int warp = warp_id(), lane = lane_id();
+  const int rank = (int)cluster_ctarank();
+  if (p.norm_w)  // RMSNorm weights of every head, read by the epilogue as broadcasts
+    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
+      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
   if (warp == 0 && lane == 0) {
-    init_bars(bars);
+    init_bars(bars, 2);
     tma_prefetch_desc(&xm);
     tma_prefetch_desc(&wm);
   }
   if (warp == 2) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // both CTAs' barriers exist before any multicast lands
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
   const int nph = (p.H + 1) >> 1;  // head pairs per block (dense phase)
-  const int n_jobs = p.dense ? p.t_q * nph : *p.n_gq;
+  const int ncp = (nph + 1) >> 1;  // cluster jobs per block (dense phase)
+  const int n_cjobs = p.dense ? p.t_q * ncp : *p.n_gqc;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int nkb = p.dm / BK;
-  auto job = [&](int w, int& i, int& h1, int& h2) {
+  // cluster job -> (block i, this CTA's heads h1/h2); false: no job for this CTA
+  // (it still loads its half of the shared x tile and releases the stages)
+  auto job = [&](int c, int& i, int& h1, int& h2) -> bool {
     if (p.dense) {
-      i = w / nph;
-      h1 = 2 * (w - i * nph);
+      i = c / ncp;
+      const int pp = 2 * (c - i * ncp) + rank;
+      h1 = 2 * pp;
       h2 = (h1 + 1 < p.H) ? h1 + 1 : -1;
-    } else {
-      const int c = p.gq_pairs[w];
-      i = c & 0xFFFF;
-      h1 = (c >> 16) & 0xFF;
-      h2 = (c >> 24) - 1;
+      return pp < nph;
     }
+    const int cj = p.gq_cjobs[c];
+    const bool mine = rank == 0 || (cj >> 30);
+    const int code = p.gq_pairs[(cj & 0x3FFFFFFF) + (mine ? rank : 0)];
+    i = code & 0xFFFF;
+    h1 = (code >> 16) & 0xFF;
+    h2 = (code >> 24) - 1;
+    return mine;
   };
 
   if (warp == 0) {
     // TMA producer (whole warp walks the schedule; one elected lane issues)
     Ring<Q_STAGES> rg;
-    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+    for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      job(w, i, h1, h2);
-      const uint32_t bytes = A_BYTES + (h2 >= 0 ? 2 : 1) * B_BYTES;
+      const bool mine = job(c, i, h1, h2);
+      const uint32_t bytes = A_BYTES + (mine ? (h2 >= 0 ? 2 : 1) * B_BYTES : 0);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
           uint8_t* st = smem + rg.s * Q_STAGE_BYTES;
           mbar_arrive_expect_tx(&bars->full[rg.s], bytes);
-          tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
-          tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h1 * BN);
-          if (h2 >= 0) tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], kb * BK, h2 * BN);
+          tma_load_2d_mc(st + rank * A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK,
+                         i * BM + rank * (BM / 2), 0x3);
+          if (mine) {
+            tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h1 * BN);
+            if (h2 >= 0)
+              tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], kb * BK, h2 * BN);
+          }
         }
         __syncwarp();
         rg.next();
       }
+    }
+    // drain: every stage released by both CTAs' MMA warps, so no arrival from the
+    // peer can target this CTA after it leaves the final cluster barrier
+    for (int k = 0; k < Q_STAGES; ++k) {
+      mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+      rg.next();
     }
   } else if (warp == 1) {
     // MMA issuer (warp-uniform schedule, elected lane issues + commits)
@@ -184,126 +217,151 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
     Ring<Q_STAGES> rg;
     int t = 0;
-    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+    for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      job(w, i, h1, h2);
+      const bool mine = job(c, i, h1, h2);
       const uint32_t idesc = h2 >= 0 ? idesc2 : idesc1;
       const int acc = t & 1;
-      mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
-      tc_fence_after();
+      if (mine) {
+        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+      }
       const uint32_t d = tbase + acc * Q_BN;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->full[rg.s], rg.ph);
         tc_fence_after();
         const uint64_t a = desc0 + (uint64_t)((rg.s * Q_STAGE_BYTES) >> 4);
         if (elect_one()) {
-          mma_kblock(d, a, a + (A_BYTES >> 4), idesc, kb > 0);
-          tc_commit(&bars->empty[rg.s]);
+          if (mine) mma_kblock(d, a, a + (A_BYTES >> 4), idesc, kb > 0);
+          tc_commit_mc(&bars->empty[rg.s], 0x3);  // the stage is free in both CTAs' view
         }
         __syncwarp();
         rg.next();
       }
-      if (elect_one()) tc_commit(&bars->tfull[acc]);
-      __syncwarp();
+      if (mine) {
+        if (elect_one()) tc_commit(&bars->tfull[acc]);
+        __syncwarp();
+        ++t;
+      }
     }
   } else if (warp >= 4) {
+    // epilogue: one accumulator row per thread. Pass 1 reads both heads' rows
+    // from TMEM for the RMS sums; pass 2 walks 32-column chunks, loading the
+    // row's rotary chunk once for both heads (prefetched a chunk ahead) and
+    // the norm weights from shared memory.
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const size_t HD = (size_t)p.H * 128;
     const bool rope = p.rope_cos != nullptr;
+    const bool norm = p.norm_w != nullptr;
+    const uint32_t nw_u32 = smem_u32(nw_smem);
     int t = 0;
-    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x, ++t) {
+    for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      job(w, i, h1, h2);
+      if (!job(c, i, h1, h2)) continue;
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
+      ++t;
       const int row = i * BM + r;
+      const bool row_ok = row < p.S;
       const int nh = h2 >= 0 ? 2 : 1;
-      const float* cs = rope ? p.rope_cos + (size_t)row * 64 : nullptr;
-      const float* sn = rope ? p.rope_sin + (size_t)row * 64 : nullptr;
-      for (int sl = 0; sl < nh; ++sl) {
-        const int h = sl ? h2 : h1;
-        uint32_t u[4][32];
-        const uint32_t ta = tbase + lane_off + acc * Q_BN + sl * BN;
-        tmem_ld32(ta + 0, u[0]);
-        tmem_ld32(ta + 32, u[1]);
-        tmem_ld32(ta + 64, u[2]);
-        tmem_ld32(ta + 96, u[3]);
-        tmem_ld_wait();
-        gemm::reg_fence(u[0]);
-        gemm::reg_fence(u[1]);
-        gemm::reg_fence(u[2]);
-        gemm::reg_fence(u[3]);
-        if (sl == nh - 1) {  // accumulator drained: release it to the MMA warp
-          tc_fence_before();
-          mbar_arrive(&bars->tempty[acc]);
-        }
-        if (row >= p.S) continue;
-        __nv_bfloat16* dst = p.q + (size_t)row * HD + (size_t)h * 128;
-        if (!p.norm_w) {
-          // plain projection (V): no normalisation, no rotary encoding
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float o[32];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[c][k]);
-            gemm::store_bf16x32(dst + c * 32, o);
-          }
-          continue;
-        }
+      const uint32_t ta0 = tbase + lane_off + acc * Q_BN;
+      float inv[2] = {1.f, 1.f};
+      if (norm) {
         // RMSNorm (tensor.py:68-80): y * w / sqrt(mean(y^2) + eps)
-        float ss = 0.f;
+        for (int sl = 0; sl < nh; ++sl) {
+          float ss = 0.f;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t u[32];
+            tmem_ld32(ta0 + sl * BN + cc * 32, u);
+            tmem_ld_wait();
+            gemm::reg_fence(u);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float v = __uint_as_float(u[c][k]);
-            ss = fmaf(v, v, ss);
+            for (int k = 0; k < 32; ++k) {
+              const float v = __uint_as_float(u[k]);
+              ss = fmaf(v, v, ss);
+            }
           }
-        const float inv = rsqrtf(ss * (1.f / 128.f) + p.eps);
-        const float* nw = p.norm_w + (size_t)h * 128;
+          inv[sl] = rsqrtf(ss * (1.f / 128.f) + p.eps);
+        }
+      }
+      const float4* cs4 = rope ? reinterpret_cast<const float4*>(p.rope_cos + (size_t)row * 64)
+                               : nullptr;
+      const float4* sn4 = rope ? reinterpret_cast<const float4*>(p.rope_sin + (size_t)row * 64)
+                               : nullptr;
+      float4 cn[4], sx[4];  // rotary chunk in flight (16 cos + 16 sin)
+      if (rope && row_ok) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int q = 0; q < 4; ++q) {
+          cn[q] = __ldg(cs4 + q);
+          sx[q] = __ldg(sn4 + q);
+        }
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        float cvv[16], svv[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          cvv[4 * q] = cn[q].x; cvv[4 * q + 1] = cn[q].y; cvv[4 * q + 2] = cn[q].z; cvv[4 * q + 3] = cn[q].w;
+          svv[4 * q] = sx[q].x; svv[4 * q + 1] = sx[q].y; svv[4 * q + 2] = sx[q].z; svv[4 * q + 3] = sx[q].w;
+        }
+        if (rope && row_ok && cc < 3) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            cn[q] = __ldg(cs4 + (cc + 1) * 4 + q);
+            sx[q] = __ldg(sn4 + (cc + 1) * 4 + q);
+          }
+        }
+        for (int sl = 0; sl < nh; ++sl) {
+          const int h = sl ? h2 : h1;
+          uint32_t u[32];
+          tmem_ld32(ta0 + sl * BN + cc * 32, u);
+          tmem_ld_wait();
+          gemm::reg_fence(u);
+          if (cc == 3 && sl == nh - 1) {  // accumulator drained: release it to the MMA warp
+            tc_fence_before();
+            mbar_arrive(&bars->tempty[acc]);
+          }
+          if (!row_ok) continue;
           float o[32];
-          // 16-byte vector loads of the norm weights and the rotary table
-          float wv[32], cvv[16], svv[16];
+          if (!norm) {
+            // plain projection (V): no normalisation, no rotary encoding
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 t4 = __ldg(reinterpret_cast<const float4*>(nw + c * 32) + q);
-            wv[4 * q] = t4.x; wv[4 * q + 1] = t4.y; wv[4 * q + 2] = t4.z; wv[4 * q + 3] = t4.w;
-          }
-          if (rope) {
+            for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[k]);
+          } else {
+            float wv[32];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 a4 = __ldg(reinterpret_cast<const float4*>(cs + c * 16) + q);
-              const float4 b4 = __ldg(reinterpret_cast<const float4*>(sn + c * 16) + q);
-              cvv[4 * q] = a4.x; cvv[4 * q + 1] = a4.y; cvv[4 * q + 2] = a4.z; cvv[4 * q + 3] = a4.w;
-              svv[4 * q] = b4.x; svv[4 * q + 1] = b4.y; svv[4 * q + 2] = b4.z; svv[4 * q + 3] = b4.w;
+            for (int q = 0; q < 8; ++q) {  // broadcast reads: every thread, same address
+              const uint4 w4 = lds128(nw_u32 + (uint32_t)((h * 128 + cc * 32 + 4 * q) * 4));
+              wv[4 * q] = __uint_as_float(w4.x); wv[4 * q + 1] = __uint_as_float(w4.y);
+              wv[4 * q + 2] = __uint_as_float(w4.z); wv[4 * q + 3] = __uint_as_float(w4.w);
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              // interleaved-pair RoPE (tensor.py:83-109)
+              const float e = __uint_as_float(u[2 * k]) * wv[2 * k] * inv[sl];
+              const float od = __uint_as_float(u[2 * k + 1]) * wv[2 * k + 1] * inv[sl];
+              if (rope) {
+                const float cv = cvv[k], sv = svv[k];
+                o[2 * k] = e * cv - od * sv;
+                o[2 * k + 1] = e * sv + od * cv;
+              } else {
+                o[2 * k] = e;
+                o[2 * k + 1] = od;
+              }
             }
           }
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            // interleaved-pair RoPE (tensor.py:83-109)
-            const float e = __uint_as_float(u[c][2 * k]) * wv[2 * k] * inv;
-            const float od = __uint_as_float(u[c][2 * k + 1]) * wv[2 * k + 1] * inv;
-            if (rope) {
-              const float cv = cvv[k], sv = svv[k];
-              o[2 * k] = e * cv - od * sv;
-              o[2 * k + 1] = e * sv + od * cv;
-            } else {
-              o[2 * k] = e;
-              o[2 * k + 1] = od;
-            }
-          }
-          gemm::store_bf16x32(dst + c * 32, o);
+          gemm::store_bf16x32(p.q + (size_t)row * HD + (size_t)h * 128 + cc * 32, o);
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
@@ -632,15 +690,39 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   }
 }
 
-void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p, int grid,
-                   cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm::Q_SMEM_BYTES);
-    configured = true;
+// launch a persistent kernel as 2-CTA clusters, as many as can be co-resident
+template <typename Kernel, typename... Args>
+static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaStream_t stream,
+                                 Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(gemm::NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (*grid_cache == 0) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0, sms = 0, clusters = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(sms & ~1);
+    if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg) != cudaSuccess || clusters < 1)
+      clusters = sms / 2;
+    *grid_cache = 2 * std::min(clusters, sms / 2);
   }
-  gemm_q_kernel<<<grid, gemm::NTHREADS, gemm::Q_SMEM_BYTES, stream>>>(xm, wm, p);
+  cfg.gridDim = dim3(*grid_cache);
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
+                   cudaStream_t stream) {
+  static int grid = 0;
+  launch_pair_clusters(gemm_q_kernel, gemm::Q_SMEM_BYTES, &grid, stream, xm, wm, p);
 }
 
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,

@@ -10,7 +10,7 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
                               // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
-                              // [4] GEMM-Q head-pair jobs
+                              // [4] GEMM-Q head-pair jobs, [5] GEMM-Q cluster jobs
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
   int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
                               // the cached tiles in the same order from index counts[1]
@@ -19,6 +19,8 @@ struct PlanView {
   long long* pairs_pred;      // [H] mask-predicted computed pairs
   int* gq_pairs;              // [H*rows] GEMM-Q jobs: block i x up to two active heads,
                               // i | h1 << 16 | (h2 + 1) << 24 (h2 = -1: single head)
+  int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: the index of the
+                              // first of up to two same-block jobs | (second exists) << 30
 };
 
 __host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
@@ -41,6 +43,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
   size_t o_ord = take((size_t)rows * sizeof(int));
   size_t o_pairs = take((size_t)H * sizeof(long long));
   size_t o_gqp = take((size_t)H * rows * sizeof(int));
+  size_t o_gqc = take((size_t)H * rows * sizeof(int));
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -49,6 +52,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->orders = reinterpret_cast<int*>(base + o_ord);
     pv->pairs_pred = reinterpret_cast<long long*>(base + o_pairs);
     pv->gq_pairs = reinterpret_cast<int*>(base + o_gqp);
+    pv->gq_cjobs = reinterpret_cast<int*>(base + o_gqc);
   }
   return off;
 }
@@ -173,14 +177,16 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
 struct GemmQParams {
   int S, dm, H, t_q, dense;
   const int* gq_pairs;  // plan head-pair jobs (sparse phase)
-  const int* n_gq;      // their count
+  const int* gq_cjobs;  // plan cluster jobs over gq_pairs (sparse phase)
+  const int* n_gqc;     // their count
   const float* norm_w;  // [H, 128]
   const float* rope_cos;  // [S, 64]
   const float* rope_sin;  // [S, 64]
   float eps;
   __nv_bfloat16* q;  // [S, H*128]
 };
-void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p, int grid,
+// persistent, one 2-CTA cluster per SM pair (grid from the co-resident cluster count)
+void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
                    cudaStream_t stream);
 
 struct GemmOParams {

@@ -261,7 +261,23 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     __syncthreads();
   }
   int jp = scan[tid] - nloc;
+  const int n_jobs_q = scan[nt - 1];
+  __syncthreads();
+  // cluster jobs: block i's jobs grouped in twos (one per CTA of a 2-CTA cluster)
+  int cloc = 0;
+  for (int i = blo; i < bhi; ++i) cloc += ((__popcll(pv.hmask[i]) + 1) / 2 + 1) / 2;
+  scan[tid] = cloc;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    int v = tid >= off ? scan[tid - off] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int jc = scan[tid] - cloc;
   for (int i = blo; i < bhi; ++i) {
+    const int nj = (__popcll(pv.hmask[i]) + 1) / 2;
+    for (int k = 0; k < nj; k += 2) pv.gq_cjobs[jc++] = (jp + k) | ((k + 1 < nj) ? (1 << 30) : 0);
     unsigned long long m = pv.hmask[i];
     while (m) {
       const int h1 = __ffsll(m) - 1;
@@ -274,7 +290,10 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
       pv.gq_pairs[jp++] = gq_pair_code(i, h1, h2);
     }
   }
-  if (tid == nt - 1) pv.counts[4] = scan[nt - 1];
+  if (tid == nt - 1) {
+    pv.counts[4] = n_jobs_q;
+    pv.counts[5] = scan[nt - 1];
+  }
 }
 
 // ---------------------------------------------------------------------------
