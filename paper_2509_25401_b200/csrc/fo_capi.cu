@@ -404,6 +404,8 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
     return rc;
   if ((rc = make_map_ex(&om, out, seq, d_model, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B, "out")))
     return rc;
+  // o moves in half tiles (64 rows), each multicast to both CTAs of a cluster
+  if ((rc = make_map(&am, o, seq, (uint64_t)heads * kTile, 64, "o"))) return rc;
   launch_gemm_o(am, bm, wm, om, p, num_sms(), (cudaStream_t)stream);
   return check_launch("gemm_o_dispatch");
 }

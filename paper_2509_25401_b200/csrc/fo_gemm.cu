@@ -392,14 +392,19 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   constexpr int TBN = UPDATE ? BN : D_BN;                     // output tile columns
   constexpr int ACC_COLS = UPDATE ? 2 * BN : D_BN;  // update: accumulator A (active) + B (cached)
   constexpr int TM_COLS = 512;
+  // dispatch runs as 2-CTA clusters: both CTAs take the same block i (hence the
+  // same K sequence of active heads) and neighbouring 256-column n-tiles; each
+  // loads half of the o tile and multicasts it to both
+  constexpr bool MC = !UPDATE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem + ST * SB;  // dispatch bias / output chunks
   Bars* bars = reinterpret_cast<Bars*>(ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES));
   const int warp = warp_id(), lane = lane_id();
+  const int rank = MC ? (int)cluster_ctarank() : 0;
   if (warp == 0 && lane == 0) {
-    init_bars(bars);
+    init_bars(bars, MC ? 2 : 1);
     tma_prefetch_desc(&am);
     tma_prefetch_desc(&cm);
     tma_prefetch_desc(&wm);
@@ -408,18 +413,30 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   if (warp == 2) tmem_alloc<TM_COLS>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();  // both CTAs' barriers exist before any multicast lands
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
   const int nbn = (p.dm + TBN - 1) / TBN;
   // columns of n-tile nb (dispatch: the last tile is 128 wide when dm % 256 != 0)
   auto tile_cols = [&](int nb) { return min(TBN, p.dm - nb * TBN); };
   const int nord = UPDATE ? p.order_d + 1 : 1;
-  const int n_jobs = p.t_q * nbn * nord;
+  const int ncb = (nbn + 1) >> 1;  // dispatch: n-tile pairs per block (one per cluster job)
+  const int n_jobs = MC ? p.t_q * ncb : p.t_q * nbn * nord;
+  const int jstart = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int jstep = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
   // job decode, order-major (all d = 0 tiles first): the static round-robin over
   // CTAs then stays balanced when the d >= 1 jobs of blocks without cached heads
   // are skipped. Returns false for update jobs with no work (d >= orders[i]).
+  // Dispatch: cluster job w = (block i, n-tile pair); false when this CTA's
+  // n-tile is past the end (it still loads its half of the shared o tile).
   auto job = [&](int w, int& i, int& nb, int& d) -> bool {
+    if (MC) {
+      i = w / ncb;
+      nb = 2 * (w - i * ncb) + rank;
+      d = 0;
+      return nb < nbn;
+    }
     const int per = p.t_q * nbn;
     d = w / per;
     const int rest = w - d * per;
@@ -434,9 +451,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   if (warp == 0) {
     {
       Ring<ST> rg;
-      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+      for (int w = jstart; w < n_jobs; w += jstep) {
         int i, nb, d;
-        if (!job(w, i, nb, d)) continue;
+        const bool mine = job(w, i, nb, d);
+        if (!MC && !mine) continue;
         const unsigned long long act = p.hmask[i];
         const unsigned long long cached = all_heads & ~act;
         // K order: [cached heads (update only)] then [active heads (d == 0 only)]
@@ -449,14 +467,20 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           while (m) {
             const int h = __ffsll(m) - 1;
             m &= m - 1;
-            const bool two = tile_cols(nb) > BN;
+            const bool two = mine && tile_cols(nb) > BN;
             for (int kk = 0; kk < 2; ++kk) {
               mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
               if (elect_one()) {
                 uint8_t* st = smem + rg.s * SB;
-                mbar_arrive_expect_tx(&bars->full[rg.s], A_BYTES + (two ? 2 : 1) * B_BYTES);
-                tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
-                tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * TBN);
+                mbar_arrive_expect_tx(&bars->full[rg.s],
+                                      A_BYTES + (mine ? (two ? 2 : 1) * B_BYTES : 0));
+                if (MC)
+                  tma_load_2d_mc(st + rank * (A_BYTES / 2), src, &bars->full[rg.s],
+                                 h * 128 + kk * BK, row0 + rank * (BM / 2), 0x3);
+                else
+                  tma_load_2d(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0);
+                if (mine)
+                  tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, nb * TBN);
                 if (two)
                   tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
                               nb * TBN + BN);
@@ -467,6 +491,11 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           }
         }
       }
+      if (MC)  // drain: both CTAs' MMA warps have released every stage
+        for (int k = 0; k < ST; ++k) {
+          mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+          rg.next();
+        }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -476,13 +505,16 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
       Ring<ST> rg;
       int t = 0;
-      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
+      for (int w = jstart; w < n_jobs; w += jstep) {
         int i, nb, d;
-        if (!job(w, i, nb, d)) continue;
-        const uint32_t idesc = tile_cols(nb) > BN ? idesc2 : idesc1;
+        const bool mine = job(w, i, nb, d);
+        if (!MC && !mine) continue;
+        const uint32_t idesc = (mine && tile_cols(nb) > BN) ? idesc2 : idesc1;
         const int acc = t & 1;
-        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
-        tc_fence_after();
+        if (mine) {
+          mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
         const unsigned long long act = p.hmask[i];
         const unsigned long long cached = all_heads & ~act;
         const uint32_t dA = tbase + acc * ACC_COLS;
@@ -497,13 +529,17 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
             tc_fence_after();
             const uint64_t a = desc0 + (uint64_t)((rg.s * SB) >> 4);
             if (elect_one()) {
-              mma_kblock(dst, a, a + (A_BYTES >> 4), idesc, kb > 0);
-              tc_commit(&bars->empty[rg.s]);
+              if (mine) mma_kblock(dst, a, a + (A_BYTES >> 4), idesc, kb > 0);
+              if (MC)
+                tc_commit_mc(&bars->empty[rg.s], 0x3);  // free in both CTAs' view
+              else
+                tc_commit(&bars->empty[rg.s]);
             }
             __syncwarp();
             rg.next();
           }
         }
+        if (!mine) continue;
         if (elect_one()) tc_commit(&bars->tfull[acc]);
         __syncwarp();
         ++t;
@@ -513,13 +549,14 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   } else if (!UPDATE && warp == 3) {
     // bias loader: 4 chunks per job through the slot ring, next job prefetched into L2
     Ring<BIAS_SLOTS> rb;
-    for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
-      const int nb = w % nbn, i = w / nbn;
+    for (int w = jstart; w < n_jobs; w += jstep) {
+      int i, nb, d;
+      if (!job(w, i, nb, d)) continue;
       const int ns = staged_orders(i);
       const int nch = tile_cols(nb) / 32;
-      const int wn = w + gridDim.x;
-      if (wn < n_jobs && elect_one()) {
-        const int nb2 = wn % nbn, i2 = wn / nbn;
+      const int wn = w + jstep;
+      int i2, nb2, d2;
+      if (wn < n_jobs && job(wn, i2, nb2, d2) && elect_one()) {
         const int ns2 = staged_orders(i2);
         for (int dd = 0; dd < ns2; ++dd)
           for (int c = 0; c < tile_cols(nb2) / 32; ++c)
@@ -594,8 +631,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       Ring<BIAS_SLOTS> rb;
       int prev = -1;  // slot of the previous chunk (released once its store has read it)
       int t = 0;
-      for (int w = blockIdx.x; w < n_jobs; w += gridDim.x) {
-        const int nb = w % nbn, i = w / nbn;
+      for (int w = jstart; w < n_jobs; w += jstep) {
+        int i, nb, d;
+        if (!job(w, i, nb, d)) continue;
         const int nch = tile_cols(nb) / 32;
         const int acc = t & 1;
         const bool hasA = p.hmask[i] != 0ull;
@@ -684,6 +722,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<TM_COLS>(tbase);
@@ -735,10 +774,13 @@ void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorM
                          gemm::SMEM_BYTES_D);
     configured = true;
   }
-  if (p.update)
+  if (p.update) {
     gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, om, p);
-  else
-    gemm_o_kernel<false><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES_D, stream>>>(am, cm, wm, om, p);
+  } else {
+    static int grid_d = 0;
+    launch_pair_clusters(gemm_o_kernel<false>, gemm::SMEM_BYTES_D, &grid_d, stream, am, cm, wm, om,
+                         p);
+  }
 }
 
 }  // namespace fo
