@@ -118,6 +118,13 @@ FO_API int fo_forecast_materialize(const void* cache, int seq, int heads, int he
                             int order_d, const void* plan_ws, const int32_t* valid,
                             const float* coef, void* out, void* stream);
 
+/* SyntheticWorkload.x(t) of the reference run() (pipeline.py:160-171) as one pass:
+ * out bf16 = bf16(f32(f64(x0) + f64(f32 terms))) with numpy's float32 products and
+ * float64 sums. kind 0 drift (c1 = t, c2 = t*t/steps), 1 poly1 (c1 = s*t),
+ * 2 poly2 (c1 = s*t, c2 = (s*t)^2); scalars already rounded to float32. */
+FO_API int fo_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
+                          float c1, float c2, float s, void* out, void* stream);
+
 /* FeatureCache.update for the selected (head, block) entries (select uint8
  * [heads, rows], NULL = all) (attention.py:71-85,128-131). */
 FO_API int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,

@@ -30,6 +30,15 @@
 #ifndef FO_CS_TC_ROWSUM
 #define FO_CS_TC_ROWSUM 0
 #endif
+// 1: no max exchange between the partner warps. Each warp reads the whole S row
+// (its own 64 columns are kept, the partner's are folded into the max only), so
+// both derive the same running max independently, and P goes to its own TMEM
+// buffer (columns 128-255) instead of over S, so no warp can clobber S the
+// partner has not read yet. Removes the per-tile shared-memory exchange and
+// the named barrier that kept the partners in lockstep.
+#ifndef FO_CS_NOXCHG
+#define FO_CS_NOXCHG 0
+#endif
 
 namespace fo {
 namespace attn_cs {
@@ -40,6 +49,8 @@ constexpr int SMEM_TILES = 1 + KST + VST;
 constexpr int NTHREADS = 384;
 constexpr int SOFTMAX_THREADS = 256;
 constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
+constexpr uint32_t TM_P0 = 128;  // FO_CS_NOXCHG: P buffers (64 columns each) at 128 / 192
+static_assert(!(FO_CS_NOXCHG && FO_CS_TC_ROWSUM), "the P buffers overlap the row-sum columns");
 constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (B operand of the row-sum MMA)
 
 struct Bars {
@@ -217,7 +228,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (j == 0 && qi > 0) mbar_wait(&bars->o_free, (qi - 1) & 1, p.status);
           mbar_wait(&bars->v_full[vst], vph, p.status);
           tc_fence_after();
-          const uint32_t a_t = tbase + TM_S0 + (pv_cnt & 1) * 128;
+          const uint32_t a_t = FO_CS_NOXCHG ? tbase + TM_P0 + (pv_cnt & 1) * 64
+                                            : tbase + TM_S0 + (pv_cnt & 1) * 128;
           const uint64_t vdesc = vdesc0 + (uint64_t)((vst * TILE_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
@@ -273,13 +285,44 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         mbar_wait(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
         tc_fence_after();
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
+        const bool mask_tail = tail && (j == n - 1);
+#if FO_CS_NOXCHG
+        float mo;  // max of the partner's columns, read here rather than exchanged
+        {
+          uint32_t w[2][32];
+          tmem_ld32(sa + (col0 ^ 64), w[0]);
+          tmem_ld32(sa + (col0 ^ 64) + 32, w[1]);
+          tmem_ld_wait();
+          reg_fence_cs(w[0]);
+          reg_fence_cs(w[1]);
+          const int colp = col0 ^ 64;
+          float pv[64];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int k = 0; k < 32; ++k) pv[c * 32 + k] = __uint_as_float(w[c][k]);
+          if (mask_tail) {
+#pragma unroll
+            for (int k = 0; k < 64; ++k)
+              if (colp + k >= last_valid) pv[k] = -INFINITY;
+          }
+          float pc[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float a = fmax3f(pv[16 * c], pv[16 * c + 1], pv[16 * c + 2]);
+#pragma unroll
+            for (int k = 3; k < 15; k += 2) a = fmax3f(a, pv[16 * c + k], pv[16 * c + k + 1]);
+            pc[c] = fmaxf(a, pv[16 * c + 15]);
+          }
+          mo = fmaxf(fmax3f(pc[0], pc[1], pc[2]), pc[3]);
+        }
+#endif
         uint32_t u[2][32];
         tmem_ld32(sa + col0, u[0]);
         tmem_ld32(sa + col0 + 32, u[1]);
         tmem_ld_wait();
         reg_fence_cs(u[0]);
         reg_fence_cs(u[1]);
-        const bool mask_tail = tail && (j == n - 1);
         float sv[64];
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -300,12 +343,16 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           mc[c] = fmaxf(a, sv[16 * c + 15]);
         }
         const float mh = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
+#if FO_CS_NOXCHG
+        (void)xmax_u32;
+#else
         const uint32_t xa = xmax_u32 + (((qk_seen & 1) * 2) * 128 + r) * 4;
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(xa + half * 512), "f"(mh) : "memory");
         // both partners have read their S halves before either overwrites S with P
         named_bar_sync(pair_bar, 64);
         float mo;
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(mo) : "r"(xa + (half ^ 1) * 512) : "memory");
+#endif
         ++qk_seen;
         const float m_tile = fmaxf(mh, mo) * p.scale_log2;
         bool need = false;
@@ -347,7 +394,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             pk[q] = pack_bf16x2(e.x, e.y);
           }
         }
+#if FO_CS_NOXCHG
+        tmem_st32(tbase + lane_off + TM_P0 + sb * 64 + half * 32, pk);
+#else
         tmem_st32(sa + half * 32, pk);
+#endif
         tmem_st_wait();
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)

@@ -288,6 +288,15 @@ int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim,
   return check_launch("forecast_materialize");
 }
 
+int fo_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind, float c1,
+                   float c2, float s, void* out, void* stream) {
+  if (!x0 || !a || !b || !out) return fail(FO_ERR_PARAM, "synthetic_x: NULL operand");
+  if (kind < 0 || kind > 2) return fail(FO_ERR_PARAM, "synthetic_x: unknown workload kind %d", kind);
+  launch_synthetic_x(x0, a, b, n, kind, c1, c2, s, static_cast<__nv_bfloat16*>(out),
+                     (cudaStream_t)stream);
+  return check_launch("synthetic_x");
+}
+
 int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,
                   int rows, int order_d, const uint8_t* select, void* stream) {
   int rc = check_head_dim(head_dim);

@@ -94,6 +94,34 @@ __global__ void cache_push_kernel(const __nv_bfloat16* __restrict__ o, __nv_bflo
   if (threadIdx.x == 0) valid[(size_t)h * t_q + i] = vn;
 }
 
+// SyntheticWorkload.x(t) (reference pipeline.py:160-171) in one pass: the
+// float32 products and float64 sums in numpy's order, rounded to float32 then
+// bf16. __fmul_rn / __fadd_rn keep nvcc from contracting into FMAs, which
+// numpy does not do. kind 0 drift, 1 poly1, 2 poly2.
+__global__ void synthetic_x_kernel(const float* __restrict__ x0, const float* __restrict__ a,
+                                   const float* __restrict__ b, size_t n, int kind, float c1,
+                                   float c2, float s, __nv_bfloat16* __restrict__ out) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    double x = (double)x0[e];
+    if (kind == 0) {  // base + s * (t * a + (t*t/steps) * b)
+      const float inner = __fadd_rn(__fmul_rn(c1, a[e]), __fmul_rn(c2, b[e]));
+      x = x + (double)__fmul_rn(s, inner);
+    } else if (kind == 1) {  // base + (s*t) * a
+      x = x + (double)__fmul_rn(c1, a[e]);
+    } else {  // base + (s*t) * a + (s*t)**2 * b
+      x = x + (double)__fmul_rn(c1, a[e]);
+      x = x + (double)__fmul_rn(c2, b[e]);
+    }
+    out[e] = __float2bfloat16_rn((float)x);
+  }
+}
+
+void launch_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
+                        float c1, float c2, float s, __nv_bfloat16* out, cudaStream_t stream) {
+  synthetic_x_kernel<<<148 * 8, 256, 0, stream>>>(x0, a, b, n, kind, c1, c2, s, out);
+}
+
 void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,
                                  const unsigned long long* hmask, const int32_t* valid,
                                  const float* coef, __nv_bfloat16* out, cudaStream_t stream) {

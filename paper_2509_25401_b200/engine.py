@@ -31,7 +31,8 @@ from dataclasses import dataclass, fields
 import numpy as np
 import torch
 
-from ._runtime import TILE, Status
+from . import _lib
+from ._runtime import TILE, Status, stream_ptr
 from .attention import FeatureCache, dense_attention_update, sparse_attention
 from .costs import StepCost, account_run
 from .errors import ParameterError
@@ -202,19 +203,17 @@ class SyntheticWorkload:
             self._dev = tuple(torch.from_numpy(a).to(dev) for a in (self.x0, self.a, self.b))
         x0, a, b = self._dev
         s = self.smoothness
-        # python scalars are weak types on both sides: fp32 products, fp64 sum
+        # python scalars are weak (float32) operands of numpy's float32 products
         if self.kind == "drift":
-            steps = max(self.config.steps, 1)
-            inner = (t * a) + ((t * t / steps) * b)
-            x = x0.double() + (s * inner).double()
+            kind, c1, c2 = 0, float(t), t * t / max(self.config.steps, 1)
         elif self.kind == "poly1":
-            x = x0.double() + ((s * t) * a).double()
+            kind, c1, c2 = 1, s * t, 0.0
         else:
-            x = x0.double() + ((s * t) * a).double() + (((s * t) ** 2) * b).double()
-        x32 = x.float()
+            kind, c1, c2 = 2, s * t, (s * t) ** 2
         if out is None:
-            return x32.to(torch.bfloat16)
-        out.copy_(x32)
+            out = torch.empty(x0.shape, dtype=torch.bfloat16, device=x0.device)
+        _lib.call("fo_synthetic_x", x0.data_ptr(), a.data_ptr(), b.data_ptr(), x0.numel(), kind,
+                  c1, c2, s, out.data_ptr(), stream_ptr(None))
         return out
 
 
@@ -259,8 +258,6 @@ class _Layer:
         self.sym = DeviceSymbols(torch.zeros(H, ceil_div(cr, 8), dtype=torch.uint8, device=device),
                                  torch.zeros(H, cr, ceil_div(cc, 8), dtype=torch.uint8,
                                              device=device), t, t, pool)
-        from . import _lib
-
         nbytes = _lib.load().fo_plan_workspace_bytes(H, t)
         # plan_g: no cache check (GEMM-Q, GEMM-O dispatch); plan_c: with the
         # cache's valid orders (attention cold-cache check, GEMM-O update orders)
