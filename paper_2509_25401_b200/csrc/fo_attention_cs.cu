@@ -30,22 +30,47 @@
 #ifndef FO_CS_TC_ROWSUM
 #define FO_CS_TC_ROWSUM 0
 #endif
+// 1 (default): row sums come out of the PV MMA itself. Every V stage carries a
+// third 64-column strip of bf16 ones after its two 64-column halves, and PV runs
+// with N = 144, so TMEM columns 128..143 accumulate l = sum(bf16(P)) next to O.
+// That costs 16/128 more PV tensor cycles (64 per tile) and removes the 32
+// packed fp32 adds per warp per tile from the FMA pipe, which (with the exp2
+// polynomial) is what bounds the softmax. The K ring drops to 2 stages to make
+// room (measured neutral).
+#ifndef FO_CS_ONESCOL
+#define FO_CS_ONESCOL 1
+#endif
+#if FO_CS_ONESCOL
+#undef FO_CS_TC_ROWSUM
+#define FO_CS_TC_ROWSUM 1  // l lives in TMEM: rescaled with O, read by the epilogue
+#ifndef FO_CS_KST
+#define FO_CS_KST 2
+#endif
+#endif
 // 1: no max exchange between the partner warps. Each warp reads the whole S row
 // (its own 64 columns are kept, the partner's are folded into the max only), so
 // both derive the same running max independently, and P goes to its own TMEM
 // buffer (columns 128-255) instead of over S, so no warp can clobber S the
 // partner has not read yet. Removes the per-tile shared-memory exchange and
 // the named barrier that kept the partners in lockstep.
+// timing experiment only (wrong results): drop the fp32 row-sum adds
+#ifndef FO_CS_NOSUM_TEST
+#define FO_CS_NOSUM_TEST 0
+#endif
 #ifndef FO_CS_NOXCHG
 #define FO_CS_NOXCHG 0
 #endif
 
 namespace fo {
 namespace attn_cs {
-constexpr int KST = 3, VST = 2;
+#ifndef FO_CS_KST
+#define FO_CS_KST 3
+#endif
+constexpr int KST = FO_CS_KST, VST = 2;
 constexpr int TILE_BYTES = kTile * kTile * 2;  // 32 KB bf16 tile
 constexpr int HALF_BYTES = TILE_BYTES / 2;     // 128 rows x 64 cols, 128B-swizzled
-constexpr int SMEM_TILES = 1 + KST + VST;
+constexpr int V_STAGE_BYTES = FO_CS_ONESCOL ? TILE_BYTES + HALF_BYTES : TILE_BYTES;
+constexpr int SMEM_TILE_BYTES = TILE_BYTES * (1 + KST) + V_STAGE_BYTES * VST;
 constexpr int NTHREADS = 384;
 constexpr int SOFTMAX_THREADS = 256;
 constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
@@ -64,7 +89,7 @@ struct Bars {
   float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
   int fc_tile;            // fused forecast: the tile the softmax warps take next
 };
-constexpr int SMEM_BYTES = SMEM_TILES * TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
+constexpr int SMEM_BYTES = SMEM_TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES <= 232448, "column-split attention exceeds shared memory");
 }  // namespace attn_cs
 
@@ -87,10 +112,15 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   uint8_t* sQ = smem;
   uint8_t* sK = smem + TILE_BYTES;
   uint8_t* sV = smem + TILE_BYTES * (1 + KST);
-  uint8_t* sOnes = smem + TILE_BYTES * SMEM_TILES;  // 1024-aligned
+  uint8_t* sOnes = smem + SMEM_TILE_BYTES;  // 1024-aligned
   Bars* bars = reinterpret_cast<Bars*>(sOnes + ONES_BYTES);
   for (int e = threadIdx.x; e < ONES_BYTES / 4; e += blockDim.x)
     reinterpret_cast<uint32_t*>(sOnes)[e] = 0x3F803F80u;  // bf16 1.0 pairs
+  if (FO_CS_ONESCOL)  // the ones strip behind each V stage (every byte 1.0, so swizzle-free)
+    for (int s = 0; s < VST; ++s)
+      for (int e = threadIdx.x; e < HALF_BYTES / 16; e += blockDim.x)
+        reinterpret_cast<uint4*>(sV + s * V_STAGE_BYTES + TILE_BYTES)[e] =
+            make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
   const int warp = warp_id(), lane = lane_id();
 
@@ -161,7 +191,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           mbar_wait(&bars->v_empty[vst], vph ^ 1, p.status);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
-            uint8_t* dv = sV + vst * TILE_BYTES;
+            uint8_t* dv = sV + vst * V_STAGE_BYTES;
             tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
             tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
           }
@@ -177,7 +207,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     {
       const uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
-      const uint32_t idesc_pv = make_idesc_bf16(128, 128, false, true);
+      // ONESCOL: N = 144 = V's 128 columns + 16 of the ones strip (row sums at 128..143)
+      const uint32_t idesc_pv = make_idesc_bf16(128, FO_CS_ONESCOL ? 144 : 128, false, true);
       const uint32_t idesc_l = make_idesc_bf16(128, 16, false, false);
       const uint64_t ones_desc = make_sdesc_sw128(smem_u32(sOnes), 16, 1024);
       (void)idesc_l;
@@ -230,13 +261,13 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           tc_fence_after();
           const uint32_t a_t = FO_CS_NOXCHG ? tbase + TM_P0 + (pv_cnt & 1) * 64
                                             : tbase + TM_S0 + (pv_cnt & 1) * 128;
-          const uint64_t vdesc = vdesc0 + (uint64_t)((vst * TILE_BYTES) >> 4);
+          const uint64_t vdesc = vdesc0 + (uint64_t)((vst * V_STAGE_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               mma_bf16_ts(tbase + TM_O, a_t + k * 8, vdesc + (uint64_t)(k * (2048 >> 4)), idesc_pv,
                           (j > 0 || k > 0));
-#if FO_CS_TC_ROWSUM
+#if FO_CS_TC_ROWSUM && !FO_CS_ONESCOL
             // row sums on the tensor core: L += P . 1, so l is exactly sum(bf16(P))
 #pragma unroll
             for (int k = 0; k < 8; ++k)
@@ -382,7 +413,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
               e.x = fast_exp2(x.x);
               e.y = fast_exp2(x.y);
             }
-            if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
+            if (!FO_CS_TC_ROWSUM && !FO_CS_NOSUM_TEST) l2 = fadd2(l2, e);
             pk[q] = pack_bf16x2(e.x, e.y);
           }
         } else {
@@ -390,7 +421,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           for (int q = 0; q < 32; ++q) {
             const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
             const float2 e = make_float2(fast_exp2(x.x), fast_exp2(x.y));  // exact zeros when masked
-            if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
+            if (!FO_CS_TC_ROWSUM && !FO_CS_NOSUM_TEST) l2 = fadd2(l2, e);
             pk[q] = pack_bf16x2(e.x, e.y);
           }
         }
