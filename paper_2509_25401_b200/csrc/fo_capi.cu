@@ -331,10 +331,12 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
     PlanView pv = plan_view(plan_ws, heads, t_q);
     p.gq_pairs = pv.gq_pairs;
     p.gq_cjobs = pv.gq_cjobs;
+    p.gq_cjobs2 = pv.gq_cjobs2;
     p.n_gqc = pv.counts + 5;
   } else {
     p.gq_pairs = nullptr;
     p.gq_cjobs = nullptr;
+    p.gq_cjobs2 = nullptr;
     p.n_gqc = nullptr;
   }
   p.norm_w = norm_w;

@@ -162,22 +162,27 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int nkb = p.dm / BK;
   // cluster job -> (block i, this CTA's heads h1/h2); false: no job for this CTA
-  // (it still loads its half of the shared x tile and releases the stages)
-  auto job = [&](int c, int& i, int& h1, int& h2) -> bool {
+  // (it still releases the stages in step with its partner). shared: both CTAs
+  // work on the same block, each loads half of the x tile and multicasts it;
+  // otherwise each loads its own x tile.
+  auto job = [&](int c, int& i, int& h1, int& h2, bool& shared) -> bool {
     if (p.dense) {
       i = c / ncp;
       const int pp = 2 * (c - i * ncp) + rank;
       h1 = 2 * pp;
       h2 = (h1 + 1 < p.H) ? h1 + 1 : -1;
+      shared = 2 * (c - i * ncp) + 1 < nph;
       return pp < nph;
     }
-    const int cj = p.gq_cjobs[c];
-    const bool mine = rank == 0 || (cj >> 30);
-    const int code = p.gq_pairs[(cj & 0x3FFFFFFF) + (mine ? rank : 0)];
+    const int j0 = p.gq_cjobs[c], j1 = p.gq_cjobs2[c];
+    const int c0 = p.gq_pairs[j0];
+    const int c1 = j1 >= 0 ? p.gq_pairs[j1] : c0;
+    shared = j1 >= 0 && (c0 & 0xFFFF) == (c1 & 0xFFFF);
+    const int code = rank ? c1 : c0;
     i = code & 0xFFFF;
     h1 = (code >> 16) & 0xFF;
     h2 = (code >> 24) - 1;
-    return mine;
+    return rank == 0 || j1 >= 0;
   };
 
   if (warp == 0) {
@@ -185,15 +190,21 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     Ring<Q_STAGES> rg;
     for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      const bool mine = job(c, i, h1, h2);
-      const uint32_t bytes = A_BYTES + (mine ? (h2 >= 0 ? 2 : 1) * B_BYTES : 0);
+      bool shared;
+      const bool mine = job(c, i, h1, h2, shared);
+      const uint32_t bytes = mine ? A_BYTES + (h2 >= 0 ? 2 : 1) * B_BYTES : 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
           uint8_t* st = smem + rg.s * Q_STAGE_BYTES;
           mbar_arrive_expect_tx(&bars->full[rg.s], bytes);
-          tma_load_2d_mc(st + rank * A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK,
-                         i * BM + rank * (BM / 2), 0x3);
+          if (shared) {
+            tma_load_2d_mc(st + rank * A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK,
+                           i * BM + rank * (BM / 2), 0x3);
+          } else if (mine) {
+            tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
+            tma_load_2d(st + A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK, i * BM + BM / 2);
+          }
           if (mine) {
             tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h1 * BN);
             if (h2 >= 0)
@@ -219,7 +230,8 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      const bool mine = job(c, i, h1, h2);
+      bool shared;
+      const bool mine = job(c, i, h1, h2, shared);
       const uint32_t idesc = h2 >= 0 ? idesc2 : idesc1;
       const int acc = t & 1;
       if (mine) {
@@ -259,7 +271,8 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      if (!job(c, i, h1, h2)) continue;
+      bool shared;
+      if (!job(c, i, h1, h2, shared)) continue;
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();

@@ -19,8 +19,8 @@ struct PlanView {
   long long* pairs_pred;      // [H] mask-predicted computed pairs
   int* gq_pairs;              // [H*rows] GEMM-Q jobs: block i x up to two active heads,
                               // i | h1 << 16 | (h2 + 1) << 24 (h2 = -1: single head)
-  int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: the index of the
-                              // first of up to two same-block jobs | (second exists) << 30
+  int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: rank 0's job index
+  int* gq_cjobs2;             // [H*rows] rank 1's job index (-1: none); same block = shared x
 };
 
 __host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
@@ -44,6 +44,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
   size_t o_pairs = take((size_t)H * sizeof(long long));
   size_t o_gqp = take((size_t)H * rows * sizeof(int));
   size_t o_gqc = take((size_t)H * rows * sizeof(int));
+  size_t o_gqc2 = take((size_t)H * rows * sizeof(int));
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -53,6 +54,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->pairs_pred = reinterpret_cast<long long*>(base + o_pairs);
     pv->gq_pairs = reinterpret_cast<int*>(base + o_gqp);
     pv->gq_cjobs = reinterpret_cast<int*>(base + o_gqc);
+    pv->gq_cjobs2 = reinterpret_cast<int*>(base + o_gqc2);
   }
   return off;
 }
@@ -177,7 +179,8 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
 struct GemmQParams {
   int S, dm, H, t_q, dense;
   const int* gq_pairs;  // plan head-pair jobs (sparse phase)
-  const int* gq_cjobs;  // plan cluster jobs over gq_pairs (sparse phase)
+  const int* gq_cjobs;  // plan cluster jobs over gq_pairs (sparse phase): rank 0's job
+  const int* gq_cjobs2;  // rank 1's job (-1: none)
   const int* n_gqc;     // their count
   const float* norm_w;  // [H, 128]
   const float* rope_cos;  // [S, 64]

@@ -263,10 +263,16 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   int jp = scan[tid] - nloc;
   const int n_jobs_q = scan[nt - 1];
   __syncthreads();
-  // cluster jobs: block i's jobs grouped in twos (one per CTA of a 2-CTA cluster)
-  int cloc = 0;
-  for (int i = blo; i < bhi; ++i) cloc += ((__popcll(pv.hmask[i]) + 1) / 2 + 1) / 2;
-  scan[tid] = cloc;
+  // cluster jobs (one job per CTA of a 2-CTA cluster): first the pairs of jobs
+  // of the same block (they share, and multicast, the x tile), then the blocks'
+  // odd jobs paired across blocks (each CTA loads its own x tile)
+  int floc = 0, sloc = 0;
+  for (int i = blo; i < bhi; ++i) {
+    const int nj = (__popcll(pv.hmask[i]) + 1) / 2;
+    floc += nj / 2;
+    sloc += nj & 1;
+  }
+  scan[tid] = floc;
   __syncthreads();
   for (int off = 1; off < nt; off <<= 1) {
     int v = tid >= off ? scan[tid - off] : 0;
@@ -274,10 +280,33 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     scan[tid] += v;
     __syncthreads();
   }
-  int jc = scan[tid] - cloc;
+  int jf = scan[tid] - floc;
+  const int n_full = scan[nt - 1];
+  __syncthreads();
+  scan[tid] = sloc;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {
+    int v = tid >= off ? scan[tid - off] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int js = scan[tid] - sloc;
+  const int n_single = scan[nt - 1];
   for (int i = blo; i < bhi; ++i) {
     const int nj = (__popcll(pv.hmask[i]) + 1) / 2;
-    for (int k = 0; k < nj; k += 2) pv.gq_cjobs[jc++] = (jp + k) | ((k + 1 < nj) ? (1 << 30) : 0);
+    for (int k = 0; k + 1 < nj; k += 2) {
+      pv.gq_cjobs[jf] = jp + k;
+      pv.gq_cjobs2[jf++] = jp + k + 1;
+    }
+    if (nj & 1) {
+      const int slot = n_full + (js >> 1);
+      if (js & 1)
+        pv.gq_cjobs2[slot] = jp + nj - 1;
+      else
+        pv.gq_cjobs[slot] = jp + nj - 1;
+      ++js;
+    }
     unsigned long long m = pv.hmask[i];
     while (m) {
       const int h1 = __ffsll(m) - 1;
@@ -292,7 +321,8 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   }
   if (tid == nt - 1) {
     pv.counts[4] = n_jobs_q;
-    pv.counts[5] = scan[nt - 1];
+    pv.counts[5] = n_full + (n_single + 1) / 2;
+    if (n_single & 1) pv.gq_cjobs2[n_full + n_single / 2] = -1;  // a lone job: rank 1 idles
   }
 }
 
