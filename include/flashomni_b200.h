@@ -118,6 +118,13 @@ FO_API int fo_forecast_materialize(const void* cache, int seq, int heads, int he
                             int order_d, const void* plan_ws, const int32_t* valid,
                             const float* coef, void* out, void* stream);
 
+/* Input validation of the reference's as_matrix (tensor.py:19-30): sets FO_ST_PARAM
+ * when any bf16 of data [rows, cols] is NaN or Inf. With plan_ws (cols = heads*128)
+ * only the tiles of active (block, head) pairs are checked, as sparse_attention
+ * checks only the q rows it reads (attention.py:194-196). */
+FO_API int fo_check_finite(const void* data, long long rows, int cols, const void* plan_ws, int heads,
+                           uint32_t* status, void* stream);
+
 /* SyntheticWorkload.x(t) of the reference run() (pipeline.py:160-171) as one pass:
  * out bf16 = bf16(f32(f64(x0) + f64(f32 terms))) with numpy's float32 products and
  * float64 sums. kind 0 drift (c1 = t, c2 = t*t/steps), 1 poly1 (c1 = s*t),

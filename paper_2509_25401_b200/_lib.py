@@ -40,6 +40,7 @@ SIGNATURES = {
     "fo_sparse_attention_reuse": [_P, _P, _P, _I, _I, _I, _P, _I, _I, _I, _P, _F, _P, _P, _I, _P,
                                   _P, _P, _P, _P],
     "fo_forecast_materialize": [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "fo_check_finite": [_P, ctypes.c_longlong, _I, _P, _I, _P, _P],
     "fo_synthetic_x": [_P, _P, _P, _SZ, _I, _F, _F, _F, _P, _P],
     "fo_cache_push": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
     "fo_gemm_q": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _F, _P, _I, _P, _P],
@@ -64,7 +65,7 @@ LAUNCHING = {n: 1 for n in ("fo_encode_symbols", "fo_decode_symbols", "fo_plan",
                             "fo_sparse_attention", "fo_sparse_attention_reuse",
                             "fo_forecast_materialize", "fo_cache_push",
                             "fo_gemm_q", "fo_gemm_o_update", "fo_gemm_o_dispatch",
-                            "fo_check_active_match", "fo_synthetic_x")}
+                            "fo_check_active_match", "fo_synthetic_x", "fo_check_finite")}
 LAUNCHING["fo_generate_masks"] = 5  # pool q, pool k, scores, cache select, skip select
 _launches = [0]
 

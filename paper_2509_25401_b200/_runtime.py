@@ -71,5 +71,25 @@ class Status:
             _lib.raise_status(bits, what)
 
 
+def check_finite(t, name, status=None, plan=None, what=None, stream=None):
+    """Reference as_matrix's finiteness check (tensor.py:19-30) on the device:
+    raises ParameterError if `t` (bf16, rows x cols) holds a NaN or Inf. With a
+    plan only the active (block, head) tiles are checked (attention.py:194-196).
+    Synchronises; called only on the checked (check=True) paths."""
+    st = status or Status.default()
+    st.check(what or name)  # surface anything already latched under its own name
+    rows = t.shape[0]
+    cols = t.numel() // max(rows, 1)
+    heads = cols // TILE if plan is not None else 0
+    _lib.call("fo_check_finite", t.data_ptr(), rows, cols, None if plan is None else plan.ptr(),
+              heads, st.ptr(), stream_ptr(stream))
+    bits = int(st.t.item())
+    if bits:
+        st.t.zero_()
+        if bits == _lib.ST_PARAM:
+            raise ParameterError(f"{name}: contains NaN or Inf")
+        _lib.raise_status(bits, what or name)
+
+
 def stream_ptr(stream=None):
     return _lib.stream_handle(stream)

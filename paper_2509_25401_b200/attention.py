@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._runtime import TILE, Status, check_bsd, require_cuda, stream_ptr
+from ._runtime import TILE, Status, check_bsd, check_finite, require_cuda, stream_ptr
 from .errors import ParameterError, ShapeError, StateError
 from .symbols import DeviceSymbols, SymbolBuffer, ceil_div
 
@@ -92,9 +92,11 @@ class FeatureCache:
         elif seq != self.seq:
             raise ShapeError(f"tile rows {seq} != cached {self.seq}")
 
-    def push(self, o, select=None, stream=None):
+    def push(self, o, select=None, stream=None, check=True):
         """Push fresh outputs o [seq, heads, 128] into every (selected) entry."""
         o = check_bsd(o, "o", heads=self.heads)
+        if check:  # update_entry's as_matrix(o_new) (attention.py:73)
+            check_finite(o, "tile", stream=stream)
         self.ensure(o.shape[0])
         sel = None
         if select is not None:
@@ -219,6 +221,11 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     if plan is None:
         plan = symbols.plan(valid=valid, valid_version=vver, order_d=order_d, status=st,
                             stream=stream, check=check)
+    if check:
+        # as_matrix (tensor.py:19-30): q only on the rows it reads (attention.py:176-196)
+        check_finite(q, "q: active-block rows", st, plan=plan, stream=stream)
+        check_finite(k, "k", st, stream=stream)
+        check_finite(v, "v", st, stream=stream)
     if out is None:
         out = torch.full((seq, heads, TILE), float(fill) if fill is not None else 0.0,
                          dtype=torch.bfloat16, device=q.device)
@@ -264,6 +271,9 @@ def dense_attention_update(q, k, v, cache, *, out=None, counters=None, stream=No
         cache.ensure(seq)
     st = status or Status.default()
     plan = _dense_plan(heads, t_q, q.device, st, stream)
+    if check:
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            check_finite(t, name, st, stream=stream)
     if out is None:
         out = torch.empty(seq, heads, TILE, dtype=torch.bfloat16, device=q.device)
     pairs = torch.zeros(heads, dtype=torch.int64, device=q.device) if counters is not None else None

@@ -288,6 +288,21 @@ int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim,
   return check_launch("forecast_materialize");
 }
 
+int fo_check_finite(const void* data, long long rows, int cols, const void* plan_ws, int heads,
+                    uint32_t* status, void* stream) {
+  if (!data || !status) return fail(FO_ERR_PARAM, "check_finite: NULL operand");
+  if (cols % 8 != 0) return fail(FO_ERR_SHAPE, "check_finite: %d columns, need a multiple of 8", cols);
+  if ((reinterpret_cast<uintptr_t>(data) & 15) != 0)
+    return fail(FO_ERR_PARAM, "check_finite: base address not 16-byte aligned");
+  const unsigned long long* hmask = nullptr;
+  if (plan_ws) {
+    if (cols != heads * kTile) return fail(FO_ERR_SHAPE, "check_finite: masked check needs H*128 columns");
+    hmask = plan_view(plan_ws, heads, ceil_div_d((int)rows, kTile)).hmask;
+  }
+  launch_check_finite(data, rows, cols, hmask, status, (cudaStream_t)stream);
+  return check_launch("check_finite");
+}
+
 int fo_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind, float c1,
                    float c2, float s, void* out, void* stream) {
   if (!x0 || !a || !b || !out) return fail(FO_ERR_PARAM, "synthetic_x: NULL operand");

@@ -117,6 +117,39 @@ __global__ void synthetic_x_kernel(const float* __restrict__ x0, const float* __
   }
 }
 
+// Input validation (reference tensor.py:19-30 as_matrix, attention.py:176-196):
+// any NaN / Inf among the bf16 values sets ST_PARAM. With `hmask`, element
+// (row, col) is checked only when head col/128 is active for block row/128
+// (cached q rows are unwritten placeholders the kernels never read). A bf16 is
+// non-finite iff its exponent bits are all ones. HBM-bound: 16-byte loads.
+__global__ void check_finite_kernel(const uint4* __restrict__ data, long long rows, int cols,
+                                    const unsigned long long* __restrict__ hmask,
+                                    uint32_t* status) {
+  const int cpr = cols / 8;  // 16-byte chunks per row
+  const long long total = rows * cpr;
+  uint32_t bad = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (hmask) {
+      const long long r = e / cpr;
+      const int h = (int)(e - r * cpr) * 8 / kTile;
+      if (!((hmask[r / kTile] >> h) & 1ull)) continue;
+    }
+    const uint4 v = __ldcs(data + e);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      bad |= ((w[q] & 0x7F80u) == 0x7F80u) | ((w[q] & 0x7F800000u) == 0x7F800000u);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_status(status, ST_PARAM);
+}
+
+void launch_check_finite(const void* data, long long rows, int cols,
+                         const unsigned long long* hmask, uint32_t* status, cudaStream_t stream) {
+  check_finite_kernel<<<148 * 8, 256, 0, stream>>>(static_cast<const uint4*>(data), rows, cols,
+                                                   hmask, status);
+}
+
 void launch_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
                         float c1, float c2, float s, __nv_bfloat16* out, cudaStream_t stream) {
   synthetic_x_kernel<<<148 * 8, 256, 0, stream>>>(x0, a, b, n, kind, c1, c2, s, out);

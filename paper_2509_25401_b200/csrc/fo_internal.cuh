@@ -209,6 +209,8 @@ void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorM
 void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,
                                  const unsigned long long* hmask, const int32_t* valid,
                                  const float* coef, __nv_bfloat16* out, cudaStream_t stream);
+void launch_check_finite(const void* data, long long rows, int cols,
+                         const unsigned long long* hmask, uint32_t* status, cudaStream_t stream);
 void launch_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
                         float c1, float c2, float s, __nv_bfloat16* out, cudaStream_t stream);
 void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,

@@ -277,12 +277,12 @@ class _Layer:
         cfg, p = self.cfg, self.params
         project_q(x, p.w_q, p.q_norm, None, "update", out=self.q, fill=None, status=status,
                   check=False)
-        project_kv(x, p, k_out=self.k, v_out=self.v)
+        project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
         tau_q = ramp_threshold(cfg.tau_q, t_step, cfg.warmup)
         tau_kv = ramp_threshold(cfg.tau_kv, t_step, cfg.warmup)
         generate_masks_heads(self.q, self.k, pool_n=cfg.pool_n, n_text=cfg.n_text, tau_q=tau_q,
                              tau_kv=tau_kv, s_q=cfg.s_q, guard=cfg.skip_guard, cache_out=self.cb,
-                             skip_out=self.sb)
+                             skip_out=self.sb, check=False)
         encode_symbols(self.cb, self.sb, cfg.pool_n, status=status, check=False, out=self.sym)
         dense_attention_update(self.q, self.k, self.v, self.cache, out=self.o, status=status,
                                check=False)
@@ -310,7 +310,7 @@ class _Layer:
         cfg, p = self.cfg, self.params
         project_q(x, p.w_q, p.q_norm, self.sym, "dispatch", out=self.q, plan=self.plan_g,
                   status=status, check=False)
-        project_kv(x, p, k_out=self.k, v_out=self.v)
+        project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
         sparse_attention(self.q, self.k, self.v, self.sym, self.cache, None, elapsed_k,
                          cfg.interval_n, cfg.order_d, mode="bias", out=self.o, plan=self.plan_c,
                          pairs=self.pairs, status=status, check=False)

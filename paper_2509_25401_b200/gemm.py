@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._runtime import TILE, Status, as_device, check_bsd, require_cuda, stream_ptr
+from ._runtime import TILE, Status, as_device, check_bsd, check_finite, require_cuda, stream_ptr
 from .attention import check_elapsed, ctypes_floats, forecast_coefficients
 from .errors import ParameterError, ShapeError, StateError
 from .symbols import DeviceSymbols, ceil_div
@@ -125,6 +125,8 @@ def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, 
         raise ShapeError(f"x width {dm} != projection input {w.d_model}")
     heads = w.heads
     t_q = ceil_div(n, TILE)
+    if check:  # gemm.py:64 as_matrix(x)
+        check_finite(x, "x", status, stream=stream)
     nw = _norm(norm_weight, heads) if norm_weight is not None else None
     cs, sn = rope_tables(n, positions, x.device) if rope else (None, None)
     if out is None:

@@ -69,13 +69,13 @@ def shard_heads(heads, world, rank):
     return list(range(rank * per, (rank + 1) * per))
 
 
-def project_kv(x, params, *, eps=1e-6, k_out=None, v_out=None, stream=None):
+def project_kv(x, params, *, eps=1e-6, k_out=None, v_out=None, stream=None, check=True):
     """Dense K (RMS norm + RoPE) and V projections (pipeline.py:223-234) on the
     GEMM-Q kernel in dense mode."""
     k = project_q(x, params.w_k, params.k_norm, None, "update", eps=eps, out=k_out, fill=None,
-                  stream=stream)
+                  stream=stream, check=check)
     v = project_q(x, params.w_v, None, None, "update", rope=False, out=v_out, fill=None,
-                  stream=stream)
+                  stream=stream, check=False)  # same x, checked once
     return k, v
 
 
@@ -94,8 +94,8 @@ def update_step(state, x, symbols_next, order_d, *, group=None, check=True, poli
     when symbols_next is None, else from the caller."""
     x = as_device(x, torch.bfloat16, "x")
     p = state.params
-    q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None)
-    k, v = project_kv(x, p)
+    q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None, check=check)
+    k, v = project_kv(x, p, check=False)
     if symbols_next is None:
         if policy is None:
             raise ParameterError("update_step needs symbols_next or a MaskPolicy")
@@ -118,7 +118,7 @@ def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check
     b = bufs or {}
     q = project_q(x, p.w_q, p.q_norm, state.symbols, "dispatch", fill=fill, out=b.get("q"),
                   check=check)
-    k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"))
+    k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"), check=False)
     o = sparse_attention(q, k, v, state.symbols, state.cache, None, elapsed_k, interval_n, order_d,
                          mode="bias", fill=fill, out=b.get("o"), check=check)
     out = project_out_dispatch(o, p.w_out, state.symbols, state.bias, elapsed_k, interval_n,

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._runtime import TILE, as_device, check_bsd, stream_ptr
+from ._runtime import TILE, as_device, check_bsd, check_finite, stream_ptr
 from .errors import ParameterError, ShapeError
 from .symbols import ceil_div, encode_symbols
 
@@ -44,7 +44,7 @@ def ramp_threshold(tau_target, step, warmup_steps):
 
 
 def generate_masks_heads(q, k, *, pool_n, n_text, tau_q, tau_kv, s_q=0.0, guard=True,
-                         cache_out=None, skip_out=None, stream=None):
+                         cache_out=None, skip_out=None, stream=None, check=True):
     """All heads at once: q, k bf16 [S, H, 128] on the device ->
     (cache_bits u8 [H, t_q], skip_bits u8 [H, t_q, t_q]), True = compute."""
     q = check_bsd(as_device(q, torch.bfloat16, "q"), "q")
@@ -59,6 +59,9 @@ def generate_masks_heads(q, k, *, pool_n, n_text, tau_q, tau_kv, s_q=0.0, guard=
                                                            device=q.device)
     if tuple(cb.shape) != (H, t_q) or tuple(sb.shape) != (H, t_q, t_q):
         raise ShapeError("generate_masks: output buffers have the wrong shape")
+    if check:  # policy.py:46-47 as_matrix(q), as_matrix(k)
+        check_finite(q, "q", stream=stream)
+        check_finite(k, "k", stream=stream)
     ws = _workspace(S, H, pool_n, q.device)
     _lib.call("fo_generate_masks", q.data_ptr(), k.data_ptr(), S, H, int(n_text), int(pool_n),
               float(tau_q), float(tau_kv), float(s_q), 1 if guard else 0, cb.data_ptr(),
@@ -111,5 +114,6 @@ class MaskPolicy:
         tq = ramp_threshold(self.tau_q, t, self.warmup)
         tkv = ramp_threshold(self.tau_kv, t, self.warmup)
         cb, sb = generate_masks_heads(q, k, pool_n=self.pool_n, n_text=self.n_text, tau_q=tq,
-                                      tau_kv=tkv, s_q=self.s_q, guard=self.guard, stream=stream)
+                                      tau_kv=tkv, s_q=self.s_q, guard=self.guard, stream=stream,
+                                      check=False)
         return encode_symbols(cb, sb, self.pool_n, stream=stream, check=False)
