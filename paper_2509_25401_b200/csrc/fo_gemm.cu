@@ -47,13 +47,17 @@ struct Bars {
   uint32_t tmem_base;
 };
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
-constexpr int SMEM_BYTES_D =
-    D_STAGES * D_STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES + 1024 + (int)sizeof(Bars);
+// output chunks are staged separately (double-buffered) so a bias slot is free
+// as soon as the epilogue has read it, not when the chunk's store has read it
+constexpr int OUT_STAGE_BYTES = BM * 32 * 2;  // 8 KB, SW64 like the bias chunks
+constexpr int SMEM_BYTES_D = D_STAGES * D_STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES +
+                             2 * OUT_STAGE_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
 // empty_count: consumers that release a stage (2 when the A tile is multicast
 // across a CTA pair: both MMA warps must be done before either producer refills)
-__device__ __forceinline__ void init_bars(Bars* b, uint32_t empty_count = 1) {
+__device__ __forceinline__ void init_bars(Bars* b, uint32_t empty_count = 1,
+                                          uint32_t bias_consumers = 1) {
   for (int s = 0; s < STAGES; ++s) {
     mbar_init(&b->full[s], 1);
     mbar_init(&b->empty[s], empty_count);
@@ -64,7 +68,7 @@ __device__ __forceinline__ void init_bars(Bars* b, uint32_t empty_count = 1) {
   }
   for (int a = 0; a < BIAS_SLOTS; ++a) {
     mbar_init(&b->bfull[a], 1);
-    mbar_init(&b->bempty[a], 1);
+    mbar_init(&b->bempty[a], bias_consumers);
   }
   fence_barrier_init();
 }
@@ -413,11 +417,12 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem + ST * SB;  // dispatch bias / output chunks
-  Bars* bars = reinterpret_cast<Bars*>(ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES));
+  uint8_t* ostage = ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES);  // dispatch out chunks
+  Bars* bars = reinterpret_cast<Bars*>(ostage + (UPDATE ? 0 : 2 * OUT_STAGE_BYTES));
   const int warp = warp_id(), lane = lane_id();
   const int rank = MC ? (int)cluster_ctarank() : 0;
   if (warp == 0 && lane == 0) {
-    init_bars(bars, MC ? 2 : 1);
+    init_bars(bars, MC ? 2 : 1, 4);  // bias slots: released by each epilogue warp
     tma_prefetch_desc(&am);
     tma_prefetch_desc(&cm);
     tma_prefetch_desc(&wm);
@@ -640,9 +645,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     } else {
       const float c0 = p.coef[0], c1 = p.coef[1], c2 = p.coef[2], c3 = p.coef[3];
       const uint32_t ring_u32 = smem_u32(ring);
+      const uint32_t ostage_u32 = smem_u32(ostage);
       const int sw = (r >> 1) & 3;  // SW64: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
       Ring<BIAS_SLOTS> rb;
-      int prev = -1;  // slot of the previous chunk (released once its store has read it)
+      int ob = 0;  // output staging buffer of this chunk
       int t = 0;
       for (int w = jstart; w < n_jobs; w += jstep) {
         int i, nb, d;
@@ -672,6 +678,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           }
           mbar_wait(&bars->bfull[rb.s], rb.ph);
           const uint32_t rowa = ring_u32 + rb.s * BIAS_SLOT_BYTES + r * 64;
+          uint4 res[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint32_t a = rowa + ((q ^ sw) << 4);
@@ -708,22 +715,29 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                 o[2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[2 * e + 1]);
               }
             }
-            sts128(a, make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
-                                 pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7])));
+            res[q] = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
+                                pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
           }
+          __syncwarp();  // this warp's rows of the bias slot are read: release it
+          if (lane == 0) mbar_arrive(&bars->bempty[rb.s]);
+          rb.next();
+          // the store that last used this staging buffer (two chunks ago) has read
+          // it: the elected thread waited for that before arriving here
+          named_bar_sync(1, 128);
+          const uint32_t orow = ostage_u32 + ob * OUT_STAGE_BYTES + r * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sts128(orow + ((q ^ sw) << 4), res[q]);
           fence_proxy_async();
           named_bar_sync(1, 128);
           if (warp == 4) {
             if (elect_one()) {
-              tma_store_2d(&om, ring + rb.s * BIAS_SLOT_BYTES, nb * TBN + c * 32, i * BM);
+              tma_store_2d(&om, ostage + ob * OUT_STAGE_BYTES, nb * TBN + c * 32, i * BM);
               bulk_commit();
-              bulk_wait_read<1>();  // the previous chunk's store has read its slot
-              if (prev >= 0) mbar_arrive(&bars->bempty[prev]);
+              bulk_wait_read<1>();  // the other staging buffer's store has read it
             }
             __syncwarp();
           }
-          prev = rb.s;
-          rb.next();
+          ob ^= 1;
         }
         ++t;
       }
