@@ -97,27 +97,6 @@ __global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uin
 // plan: one CTA turns the symbols of a layer into the schedules the hot-path
 // kernels consume. Everything here is integer work on a few KB.
 // ---------------------------------------------------------------------------
-__device__ int row_popcount(const uint8_t* row, int comp_cols, int cols, int pool_n) {
-  int cnt = 0;
-  const int nbytes = ceil_div_d(comp_cols, 8);
-  for (int b = 0; b < nbytes; ++b) {
-    uint32_t byte = row[b];
-    int nvalid = min(8, comp_cols - b * 8);
-    byte &= (0xFFu << (8 - nvalid)) & 0xFFu;  // ignore padding bits (decode_run truncates)
-    if (pool_n == 1) {
-      cnt += __popc(byte);
-    } else {
-      while (byte) {
-        int k = __clz(byte) - 24;  // MSB-first bit index
-        byte &= ~(0x80u >> k);
-        int c = b * 8 + k;
-        cnt += min(pool_n, cols - c * pool_n);
-      }
-    }
-  }
-  return cnt;
-}
-
 __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
@@ -129,7 +108,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   const int nseg = (H * (cols + 2) + 1024) * (int)sizeof(int) <= 160 * 1024 ? H : 1;
   int* hist = plan_smem;                   // [nseg][cols + 2] -> exclusive offsets
   int* scan = hist + nseg * (cols + 2);    // [1024]
-  __shared__ unsigned long long s_pairs[64];
+  __shared__ unsigned int s_pairs[64];  // per-head pairs <= 2048 x 2048: 32-bit (native shared atomics)
   const int comp_rows = ceil_div_d(rows, pool_n), comp_cols = ceil_div_d(cols, pool_n);
   const int sc_len = ceil_div_d(comp_rows, 8), row_stride = ceil_div_d(comp_cols, 8);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -142,11 +121,6 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
 
   auto is_active = [&](int h, int i) -> int {
     return dense ? 1 : (int)decode_spatial(s_c + (size_t)h * sc_len, i, pool_n);
-  };
-  auto kv_count = [&](int h, int i) -> int {
-    if (dense) return cols;
-    return row_popcount(s_s + ((size_t)h * comp_rows + i / pool_n) * row_stride, comp_cols, cols,
-                        pool_n);
   };
 
   // pass 1: histogram of per-row KV counts, head masks, checks
@@ -172,16 +146,54 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     }
     pv.orders[i] = no;
   }
+  // per-(head, block) KV counts, computed once and kept in gq_cjobs2 (free until
+  // pass 4) for pass 2. The row's bytes are loaded 8 at a time before use, so a
+  // row costs a few load latencies instead of one per byte.
+  int* kvc = pv.gq_cjobs2;
+  for (int idx = tid; idx < total; idx += nt) {
+    const int h = idx / rows, i = idx % rows;
+    int c = -1;
+    if (dense) {
+      c = cols;
+    } else if (is_active(h, i)) {
+      const uint8_t* row = s_s + ((size_t)h * comp_rows + i / pool_n) * row_stride;
+      c = 0;
+      for (int b0 = 0; b0 < row_stride; b0 += 8) {
+        uint32_t by[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) by[k] = (b0 + k < row_stride) ? row[b0 + k] : 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int b = b0 + k;
+          if (b >= row_stride) break;
+          uint32_t byte = by[k];
+          const int nvalid = min(8, comp_cols - b * 8);
+          byte &= (0xFFu << (8 - nvalid)) & 0xFFu;  // padding bits (decode_run truncates)
+          if (pool_n == 1) {
+            c += __popc(byte);
+          } else {
+            while (byte) {
+              const int kk = __clz(byte) - 24;  // MSB-first bit index
+              byte &= ~(0x80u >> kk);
+              c += min(pool_n, cols - (b * 8 + kk) * pool_n);
+            }
+          }
+        }
+      }
+    }
+    kvc[idx] = c;
+  }
+  __syncthreads();
   for (int idx = tid; idx < total; idx += nt) {
     int h = idx / rows, i = idx % rows;
     if (is_active(h, i)) {
-      int cnt = kv_count(h, i);
+      int cnt = kvc[idx];
       if (cnt == 0) {
         // active query block with every key block skipped (pyref.py:43-46)
         raise_status(status, ST_CONSISTENCY);
       } else {
         atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
-        atomicAdd(&s_pairs[h], (unsigned long long)cnt);
+        atomicAdd(&s_pairs[h], (unsigned int)cnt);
       }
     } else if (valid && valid[(size_t)h * rows + i] < 1) {
       // cached tile with a cold cache (attention.py:208-211)
@@ -189,28 +201,54 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     }
   }
   __syncthreads();
-  // exclusive scan: segment-major, descending KV count within a segment
-  if (tid == 0) {
-    int run = 0;
-    for (int g = 0; g < nseg; ++g)
-      for (int c = cols; c >= 1; --c) {
-        const int n = hist[g * (cols + 2) + c];
-        hist[g * (cols + 2) + c] = run;
+  // exclusive scan: segment-major, descending KV count within a segment. One
+  // warp per segment scans it in 32-wide chunks (shuffle scan), then the
+  // segment totals are scanned and added back (a single-thread walk over
+  // H*(cols+1) counters took ~100 us at C4).
+  {
+    const int wid = tid >> 5, ln = tid & 31, nw = nt >> 5;
+    int* seg_tot = scan;  // [nseg] (scan[] is free until pass 3)
+    for (int g = wid; g < nseg; g += nw) {
+      int run = 0;
+      for (int c0 = cols; c0 >= 1; c0 -= 32) {
+        const int c = c0 - ln;
+        const int v = c >= 1 ? hist[g * (cols + 2) + c] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (ln >= o) x += y;
+        }
+        if (c >= 1) hist[g * (cols + 2) + c] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (ln == 0) seg_tot[g] = run;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int g = 0; g < nseg; ++g) {
+        const int n = seg_tot[g];
+        seg_tot[g] = run;
         run += n;
       }
-    pv.counts[0] = run;  // attention items
+      pv.counts[0] = run;  // attention items
+    }
+    __syncthreads();
+    for (int e = tid; e < nseg * (cols + 2); e += nt) {
+      const int g = e / (cols + 2), c = e - g * (cols + 2);
+      if (c >= 1 && c <= cols) hist[e] += seg_tot[g];
+    }
   }
   for (int h = tid; h < H; h += nt) pv.pairs_pred[h] = (long long)s_pairs[h];
   __syncthreads();
   // pass 2: scatter attention items (sorted by KV count, descending)
   for (int idx = tid; idx < total; idx += nt) {
-    int h = idx / rows, i = idx % rows;
-    if (is_active(h, i)) {
-      int cnt = kv_count(h, i);
-      if (cnt > 0) {
-        int pos = atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
-        pv.items[pos] = make_int2((h << 20) | i, cnt);
-      }
+    const int cnt = kvc[idx];  // -1 cached, 0 empty (flagged above)
+    if (cnt > 0) {
+      const int h = idx / rows, i = idx % rows;
+      int pos = atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
+      pv.items[pos] = make_int2((h << 20) | i, cnt);
     }
   }
   // pass 3: GEMM-Q tile list in (block, head) order: compaction via block scan
