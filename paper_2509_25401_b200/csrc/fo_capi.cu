@@ -70,6 +70,16 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
 // Attention kernel: the column-split softmax kernel (fo_attention_cs.cu) by
 // default; FO_ATTN_IMPL=v1 selects the single-warpgroup one (read once per
 // process; both meet the same parity tests)
+// Dense GEMM-Q on CTA pairs (cta_group::2); FO_GEMM_2SM=0 selects the 1-CTA kernel.
+bool gemm_2sm_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FO_GEMM_2SM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int attention_impl() {
   static int impl = -1;
   if (impl < 0) {
@@ -359,7 +369,13 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   p.rope_sin = rope_sin;
   p.eps = eps;
   p.q = static_cast<__nv_bfloat16*>(q_out);
-  launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
+  if (dense && heads % 2 == 0 && gemm_2sm_enabled()) {
+    CUtensorMap xm2;  // full 128-row x tiles (no multicast on the CTA-pair path)
+    if ((rc = make_map(&xm2, x, seq, d_model, 128, "x"))) return rc;
+    launch_gemm_q2(xm2, wm, p, (cudaStream_t)stream);
+  } else {
+    launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
+  }
   return check_launch("gemm_q");
 }
 

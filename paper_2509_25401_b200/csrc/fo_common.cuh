@@ -125,6 +125,9 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return d;
 }
 
+#ifndef FO_EXP2_POLY_DEG
+#define FO_EXP2_POLY_DEG 3
+#endif
 // 2^x on the FMA pipe (offloads the MUFU): x = j + f, j = floor(x) taken from the
 // mantissa of x + 1.5*2^23 rounded down, 2^f by a degree-3 minimax polynomial
 // (max rel err 8.7e-5, far below the bf16 rounding P gets), exponent added as an
@@ -136,9 +139,15 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   const float2 t = fadd2_rm(x, magic);
   const float2 j = fsub2(t, magic);
   const float2 f = fsub2(x, j);
+#if FO_EXP2_POLY_DEG == 2
+  // degree 2 (max rel err 1.7e-3, below the 3.9e-3 bf16 rounding P gets anyway)
+  float2 p = ffma2(f, make_float2(0.33718943f, 0.33718943f), make_float2(0.65763628f, 0.65763628f));
+  p = ffma2(p, f, make_float2(1.00172476f, 1.00172476f));
+#else
   float2 p = ffma2(f, make_float2(0.07705805f, 0.07705805f), make_float2(0.22764557f, 0.22764557f));
   p = ffma2(p, f, make_float2(0.69512289f, 0.69512289f));
   p = ffma2(p, f, make_float2(1.f, 1.f));
+#endif
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
@@ -358,6 +367,57 @@ __device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- CTA pair (cta_group::2): one MMA over both CTAs' shared memory and TMEM.
+// The even CTA of the pair issues; A rows and B columns are split between the
+// two CTAs at the same shared-memory offsets (cute SM100_MMA_F16BF16_2x1SM_SS).
+__device__ __forceinline__ void mma_bf16_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of `mask` when the pair's MMAs complete
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// TMA load into this CTA's shared memory that completes tx on the even CTA's
+// mbarrier (peer bit cleared, cute SM100_TMA_2SM_LOAD)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_dst)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+// arrive on the mbarrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {

@@ -114,6 +114,35 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 }
 }  // namespace gemm
 
+// launch a persistent kernel as 2-CTA clusters, as many as can be co-resident
+template <typename Kernel, typename... Args>
+static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaStream_t stream,
+                                 Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(gemm::NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (*grid_cache == 0) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0, sms = 0, clusters = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(sms & ~1);
+    if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg) != cudaSuccess || clusters < 1)
+      clusters = sms / 2;
+    *grid_cache = 2 * std::min(clusters, sms / 2);
+  }
+  cfg.gridDim = dim3(*grid_cache);
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // =============================================================================
 // GEMM-Q
 // =============================================================================
@@ -133,6 +162,110 @@ constexpr int Q_NW_BYTES = 64 * 128 * 4;  // RMSNorm weights of up to 64 heads
 constexpr int Q_SMEM_BYTES = Q_STAGES * Q_STAGE_BYTES + 1024 + 1024 + Q_NW_BYTES;
 constexpr int A_HALF_BYTES = A_BYTES / 2;  // 64 rows x 64 K, SW128
 static_assert(Q_SMEM_BYTES <= 232448, "GEMM-Q shared memory over the sm_100 limit");
+}  // namespace gemm
+
+namespace gemm {
+// GEMM-Q epilogue of one job for accumulator row r (one thread per row):
+// pass 1 reads both heads' rows from TMEM for the RMS sums; pass 2 walks
+// 32-column chunks, loading the row's rotary chunk once for both heads
+// (prefetched a chunk ahead) and the norm weights from shared memory.
+// release() hands the accumulator back to the MMA warp after its last read.
+template <typename Release>
+__device__ __forceinline__ void q_epilogue_job(const GemmQParams& p, uint32_t ta0, int r, int i,
+                                               int h1, int h2, uint32_t nw_u32, Release release) {
+  const size_t HD = (size_t)p.H * 128;
+  const bool rope = p.rope_cos != nullptr;
+  const bool norm = p.norm_w != nullptr;
+  const int row = i * BM + r;
+  const bool row_ok = row < p.S;
+  const int nh = h2 >= 0 ? 2 : 1;
+  float inv[2] = {1.f, 1.f};
+  if (norm) {
+    // RMSNorm (tensor.py:68-80): y * w / sqrt(mean(y^2) + eps)
+    for (int sl = 0; sl < nh; ++sl) {
+      float ss = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t u[32];
+        tmem_ld32(ta0 + sl * BN + cc * 32, u);
+        tmem_ld_wait();
+        gemm::reg_fence(u);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float v = __uint_as_float(u[k]);
+          ss = fmaf(v, v, ss);
+        }
+      }
+      inv[sl] = rsqrtf(ss * (1.f / 128.f) + p.eps);
+    }
+  }
+  const float4* cs4 = rope ? reinterpret_cast<const float4*>(p.rope_cos + (size_t)row * 64)
+                           : nullptr;
+  const float4* sn4 = rope ? reinterpret_cast<const float4*>(p.rope_sin + (size_t)row * 64)
+                           : nullptr;
+  float4 cn[4], sx[4];  // rotary chunk in flight (16 cos + 16 sin)
+  if (rope && row_ok) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cn[q] = __ldg(cs4 + q);
+      sx[q] = __ldg(sn4 + q);
+    }
+  }
+#pragma unroll 1
+  for (int cc = 0; cc < 4; ++cc) {
+    float cvv[16], svv[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cvv[4 * q] = cn[q].x; cvv[4 * q + 1] = cn[q].y; cvv[4 * q + 2] = cn[q].z; cvv[4 * q + 3] = cn[q].w;
+      svv[4 * q] = sx[q].x; svv[4 * q + 1] = sx[q].y; svv[4 * q + 2] = sx[q].z; svv[4 * q + 3] = sx[q].w;
+    }
+    if (rope && row_ok && cc < 3) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cn[q] = __ldg(cs4 + (cc + 1) * 4 + q);
+        sx[q] = __ldg(sn4 + (cc + 1) * 4 + q);
+      }
+    }
+    for (int sl = 0; sl < nh; ++sl) {
+      const int h = sl ? h2 : h1;
+      uint32_t u[32];
+      tmem_ld32(ta0 + sl * BN + cc * 32, u);
+      tmem_ld_wait();
+      gemm::reg_fence(u);
+      if (cc == 3 && sl == nh - 1) release();  // accumulator drained
+      if (!row_ok) continue;
+      float o[32];
+      if (!norm) {
+        // plain projection (V): no normalisation, no rotary encoding
+#pragma unroll
+        for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[k]);
+      } else {
+        float wv[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // broadcast reads: every thread, same address
+          const uint4 w4 = lds128(nw_u32 + (uint32_t)((h * 128 + cc * 32 + 4 * q) * 4));
+          wv[4 * q] = __uint_as_float(w4.x); wv[4 * q + 1] = __uint_as_float(w4.y);
+          wv[4 * q + 2] = __uint_as_float(w4.z); wv[4 * q + 3] = __uint_as_float(w4.w);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          // interleaved-pair RoPE (tensor.py:83-109)
+          const float e = __uint_as_float(u[2 * k]) * wv[2 * k] * inv[sl];
+          const float od = __uint_as_float(u[2 * k + 1]) * wv[2 * k + 1] * inv[sl];
+          if (rope) {
+            const float cv = cvv[k], sv = svv[k];
+            o[2 * k] = e * cv - od * sv;
+            o[2 * k + 1] = e * sv + od * cv;
+          } else {
+            o[2 * k] = e;
+            o[2 * k + 1] = od;
+          }
+        }
+      }
+      gemm::store_bf16x32(p.q + (size_t)row * HD + (size_t)h * 128 + cc * 32, o);
+    }
+  }
+}
 }  // namespace gemm
 
 __global__ void __launch_bounds__(gemm::NTHREADS, 1)
@@ -268,9 +401,6 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    const size_t HD = (size_t)p.H * 128;
-    const bool rope = p.rope_cos != nullptr;
-    const bool norm = p.norm_w != nullptr;
     const uint32_t nw_u32 = smem_u32(nw_smem);
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl) {
@@ -281,99 +411,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
       ++t;
-      const int row = i * BM + r;
-      const bool row_ok = row < p.S;
-      const int nh = h2 >= 0 ? 2 : 1;
-      const uint32_t ta0 = tbase + lane_off + acc * Q_BN;
-      float inv[2] = {1.f, 1.f};
-      if (norm) {
-        // RMSNorm (tensor.py:68-80): y * w / sqrt(mean(y^2) + eps)
-        for (int sl = 0; sl < nh; ++sl) {
-          float ss = 0.f;
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t u[32];
-            tmem_ld32(ta0 + sl * BN + cc * 32, u);
-            tmem_ld_wait();
-            gemm::reg_fence(u);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const float v = __uint_as_float(u[k]);
-              ss = fmaf(v, v, ss);
-            }
-          }
-          inv[sl] = rsqrtf(ss * (1.f / 128.f) + p.eps);
-        }
-      }
-      const float4* cs4 = rope ? reinterpret_cast<const float4*>(p.rope_cos + (size_t)row * 64)
-                               : nullptr;
-      const float4* sn4 = rope ? reinterpret_cast<const float4*>(p.rope_sin + (size_t)row * 64)
-                               : nullptr;
-      float4 cn[4], sx[4];  // rotary chunk in flight (16 cos + 16 sin)
-      if (rope && row_ok) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          cn[q] = __ldg(cs4 + q);
-          sx[q] = __ldg(sn4 + q);
-        }
-      }
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        float cvv[16], svv[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          cvv[4 * q] = cn[q].x; cvv[4 * q + 1] = cn[q].y; cvv[4 * q + 2] = cn[q].z; cvv[4 * q + 3] = cn[q].w;
-          svv[4 * q] = sx[q].x; svv[4 * q + 1] = sx[q].y; svv[4 * q + 2] = sx[q].z; svv[4 * q + 3] = sx[q].w;
-        }
-        if (rope && row_ok && cc < 3) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            cn[q] = __ldg(cs4 + (cc + 1) * 4 + q);
-            sx[q] = __ldg(sn4 + (cc + 1) * 4 + q);
-          }
-        }
-        for (int sl = 0; sl < nh; ++sl) {
-          const int h = sl ? h2 : h1;
-          uint32_t u[32];
-          tmem_ld32(ta0 + sl * BN + cc * 32, u);
-          tmem_ld_wait();
-          gemm::reg_fence(u);
-          if (cc == 3 && sl == nh - 1) {  // accumulator drained: release it to the MMA warp
-            tc_fence_before();
-            mbar_arrive(&bars->tempty[acc]);
-          }
-          if (!row_ok) continue;
-          float o[32];
-          if (!norm) {
-            // plain projection (V): no normalisation, no rotary encoding
-#pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(u[k]);
-          } else {
-            float wv[32];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {  // broadcast reads: every thread, same address
-              const uint4 w4 = lds128(nw_u32 + (uint32_t)((h * 128 + cc * 32 + 4 * q) * 4));
-              wv[4 * q] = __uint_as_float(w4.x); wv[4 * q + 1] = __uint_as_float(w4.y);
-              wv[4 * q + 2] = __uint_as_float(w4.z); wv[4 * q + 3] = __uint_as_float(w4.w);
-            }
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              // interleaved-pair RoPE (tensor.py:83-109)
-              const float e = __uint_as_float(u[2 * k]) * wv[2 * k] * inv[sl];
-              const float od = __uint_as_float(u[2 * k + 1]) * wv[2 * k + 1] * inv[sl];
-              if (rope) {
-                const float cv = cvv[k], sv = svv[k];
-                o[2 * k] = e * cv - od * sv;
-                o[2 * k + 1] = e * sv + od * cv;
-              } else {
-                o[2 * k] = e;
-                o[2 * k + 1] = od;
-              }
-            }
-          }
-          gemm::store_bf16x32(p.q + (size_t)row * HD + (size_t)h * 128 + cc * 32, o);
-        }
-      }
+      gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, [&]() {
+        tc_fence_before();
+        mbar_arrive(&bars->tempty[acc]);
+      });
     }
   }
   tc_fence_before();
@@ -383,6 +424,149 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
+}
+
+// =============================================================================
+// GEMM-Q dense phase on CTA pairs (cta_group::2): the update-step Q and the K / V
+// projections. A cluster job is two query blocks x two heads, one 256 x 256
+// tcgen05 tile over both SMs: each CTA loads its own 128 x-rows and its own
+// head's 128 W-rows per k-block, and the even CTA issues M=256 / N=256 MMAs that
+// read both CTAs' shared memory and write 128 rows to each CTA's TMEM. The feed
+// is 64 B per MMA cycle per SM (96 for the 1-CTA 128 x 256 tile). Needs an even
+// head count; the plan-driven sparse phase stays on gemm_q_kernel.
+// =============================================================================
+namespace gemm {
+constexpr int Q2_STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KB per CTA
+constexpr int Q2_STAGES = 6;
+constexpr int Q2_SMEM_BYTES = Q2_STAGES * Q2_STAGE_BYTES + 1024 + 1024 + Q_NW_BYTES;
+static_assert(Q2_SMEM_BYTES <= 232448, "2-CTA GEMM-Q shared memory over the sm_100 limit");
+}  // namespace gemm
+
+__global__ void __launch_bounds__(gemm::NTHREADS, 1)
+    gemm_q2_kernel(const __grid_constant__ CUtensorMap xm,  // x, box 64 K x 128 rows
+                   const __grid_constant__ CUtensorMap wm, const GemmQParams p) {
+  using namespace gemm;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + Q2_STAGES * Q2_STAGE_BYTES);
+  float* nw_smem = reinterpret_cast<float*>(smem + Q2_STAGES * Q2_STAGE_BYTES + 1024);
+  const int warp = warp_id(), lane = lane_id();
+  const int rank = (int)cluster_ctarank();
+  if (p.norm_w)
+    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
+      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bars->full[s], 1);   // the even CTA's producer arrives (tx from both CTAs)
+      mbar_init(&bars->empty[s], 1);  // the pair's MMA commit reaches both CTAs
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&bars->tfull[a], 1);
+      mbar_init(&bars->tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&xm);
+    tma_prefetch_desc(&wm);
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+  const int nph = p.H >> 1;                    // head pairs
+  const int nbp = (p.t_q + 1) >> 1;            // block pairs
+  const int n_cjobs = nbp * nph;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nkb = p.dm / BK;
+  auto job = [&](int c, int& i, int& h1, int& h2) {  // block-pair-major
+    const int bp = c / nph;
+    i = 2 * bp + rank;
+    h1 = 2 * (c - bp * nph);
+    h2 = h1 + 1;
+  };
+
+  if (warp == 0) {
+    // both CTAs load their own x rows and their own head's W rows; the bytes
+    // land on the even CTA's full barrier
+    Ring<Q2_STAGES> rg;
+    for (int c = cid; c < n_cjobs; c += ncl) {
+      int i, h1, h2;
+      job(c, i, h1, h2);
+      const int hh = rank ? h2 : h1;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+        if (elect_one()) {
+          uint8_t* st = smem + rg.s * Q2_STAGE_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&bars->full[rg.s], 2 * Q2_STAGE_BYTES);
+          tma_load_2d_2sm(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
+          tma_load_2d_2sm(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, hh * BN);
+        }
+        __syncwarp();
+        rg.next();
+      }
+    }
+  } else if (warp == 1 && rank == 0) {
+    // MMA issuer of the pair
+    const uint32_t idesc = make_idesc_bf16(2 * BM, Q_BN, false, false);
+    const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
+    Ring<Q2_STAGES> rg;
+    int t = 0;
+    for (int c = cid; c < n_cjobs; c += ncl, ++t) {
+      const int acc = t & 1;
+      mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tbase + acc * Q_BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&bars->full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint64_t a = desc0 + (uint64_t)((rg.s * Q2_STAGE_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss_2sm(d, a + 2 * k, a + (A_BYTES >> 4) + 2 * k, idesc,
+                            (kb > 0 || k > 0) ? 1u : 0u);
+          tc_commit_2sm_mc(&bars->empty[rg.s], 0x3);
+        }
+        __syncwarp();
+        rg.next();
+      }
+      if (elect_one()) tc_commit_2sm_mc(&bars->tfull[acc], 0x3);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t nw_u32 = smem_u32(nw_smem);
+    int t = 0;
+    for (int c = cid; c < n_cjobs; c += ncl, ++t) {
+      int i, h1, h2;
+      job(c, i, h1, h2);
+      const int acc = t & 1;
+      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&bars->tempty[acc], 0);
+      });
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<512>(tbase);
+  }
+}
+
+void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
+                    cudaStream_t stream) {
+  static int grid = 0;
+  launch_pair_clusters(gemm_q2_kernel, gemm::Q2_SMEM_BYTES, &grid, stream, xm, wm, p);
 }
 
 // =============================================================================
@@ -754,35 +938,6 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc<TM_COLS>(tbase);
   }
-}
-
-// launch a persistent kernel as 2-CTA clusters, as many as can be co-resident
-template <typename Kernel, typename... Args>
-static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaStream_t stream,
-                                 Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(gemm::NTHREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (*grid_cache == 0) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int dev = 0, sms = 0, clusters = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cfg.gridDim = dim3(sms & ~1);
-    if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg) != cudaSuccess || clusters < 1)
-      clusters = sms / 2;
-    *grid_cache = 2 * std::min(clusters, sms / 2);
-  }
-  cfg.gridDim = dim3(*grid_cache);
-  cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,

@@ -191,6 +191,9 @@ struct GemmQParams {
 // persistent, one 2-CTA cluster per SM pair (grid from the co-resident cluster count)
 void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
                    cudaStream_t stream);
+// dense phase on CTA pairs (cta_group::2); xm with a 128-row box, even head count
+void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
+                    cudaStream_t stream);
 
 struct GemmOParams {
   int S, dm, H, t_q, order_d;
