@@ -152,12 +152,16 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
   const int n_items = *p.n_items;
+  const int n_waves = *p.n_waves;  // plan schedule: CTA b's k-th item is sched[k * grid + b]
+  (void)n_items;
   const size_t head_sym = (size_t)p.comp_rows * p.row_stride;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+    for (int k = 0; k < n_waves; ++k, ++qi) {
+      const int w = p.sched[k * gridDim.x + blockIdx.x];
+      if (w < 0) break;
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF;
       mbar_wait(&bars->q_empty, (qi & 1) ^ 1, p.status);
@@ -244,7 +248,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (elect_one()) tc_commit(&bars->q_empty);
         __syncwarp();
       };
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+      for (int k = 0; k < n_waves; ++k, ++qi) {
+        const int w = p.sched[k * gridDim.x + blockIdx.x];
+        if (w < 0) break;
         const int n = p.items[w].y;
         mbar_wait(&bars->q_full, qi & 1, p.status);
         tc_fence_after();
@@ -302,7 +308,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t qk_seen = 0, o_base = 0;
     int qi = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++qi) {
+    for (int k = 0; k < n_waves; ++k, ++qi) {
+      const int w = p.sched[k * gridDim.x + blockIdx.x];
+      if (w < 0) break;
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF, n = it.y;
       const bool tail = (last_valid < kTile) &&

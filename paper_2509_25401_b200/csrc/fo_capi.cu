@@ -182,16 +182,18 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
   if (rc) return rc;
   if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
   PlanView pv = plan_view(plan_ws, heads, rows);
-  const bool head_major = (size_t)(heads * (cols + 2) + 1024) * sizeof(int) <= 160 * 1024;
-  const size_t smem = (size_t)((head_major ? heads : 1) * (cols + 2) + 1024) * sizeof(int);
+  // hist [nseg][cols+2] + scan [1024] + bin_of_rank [1024] + wave_len [1024]
+  const bool head_major = (size_t)(heads * (cols + 2) + 3072) * sizeof(int) <= 160 * 1024;
+  const size_t smem = (size_t)((head_major ? heads : 1) * (cols + 2) + 3072) * sizeof(int);
   if (smem > 200 * 1024) return fail(FO_ERR_PARAM, "too many key blocks (%d)", cols);
+  if (num_sms() > 256) return fail(FO_ERR_CUDA, "the balanced schedule supports up to 256 SMs");
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
-                                                       valid, order_d, pv, status);
+                                                       valid, order_d, num_sms(), pv, status);
   return check_launch("plan");
 }
 
@@ -231,6 +233,8 @@ static int attention_common(const void* q, const void* k, const void* v, int seq
   p.s_s = s_s;
   p.items = pv.items;
   p.n_items = pv.counts;
+  p.sched = pv.att_sched;
+  p.n_waves = pv.counts + 6;
   p.out = static_cast<__nv_bfloat16*>(out);
   p.cache = update_mode ? static_cast<__nv_bfloat16*>(cache) : nullptr;
   p.valid = update_mode ? valid : nullptr;

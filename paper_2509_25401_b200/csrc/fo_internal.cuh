@@ -10,7 +10,8 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
                               // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
-                              // [4] GEMM-Q head-pair jobs, [5] GEMM-Q cluster jobs
+                              // [4] GEMM-Q head-pair jobs, [5] GEMM-Q cluster jobs,
+                              // [6] attention waves of the balanced schedule
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
   int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
                               // the cached tiles in the same order from index counts[1]
@@ -21,6 +22,7 @@ struct PlanView {
                               // i | h1 << 16 | (h2 + 1) << 24 (h2 = -1: single head)
   int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: rank 0's job index
   int* gq_cjobs2;             // [H*rows] rank 1's job index (-1: none); same block = shared x
+  int* att_sched;             // [H*rows + 1024] attention item of (wave k, CTA b) at k*P + b, -1 none
 };
 
 __host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
@@ -45,6 +47,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
   size_t o_gqp = take((size_t)H * rows * sizeof(int));
   size_t o_gqc = take((size_t)H * rows * sizeof(int));
   size_t o_gqc2 = take((size_t)H * rows * sizeof(int));
+  size_t o_sched = take(((size_t)H * rows + 1024) * sizeof(int));
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -55,6 +58,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->gq_pairs = reinterpret_cast<int*>(base + o_gqp);
     pv->gq_cjobs = reinterpret_cast<int*>(base + o_gqc);
     pv->gq_cjobs2 = reinterpret_cast<int*>(base + o_gqc2);
+    pv->att_sched = reinterpret_cast<int*>(base + o_sched);
   }
   return off;
 }
@@ -65,8 +69,8 @@ __global__ void encode_symbols_kernel(const uint8_t* cache_bits, const uint8_t* 
 __global__ void decode_symbols_kernel(const uint8_t* s_c, const uint8_t* s_s, int H, int rows,
                                       int cols, int pool_n, uint8_t* active, uint8_t* pair_bits);
 __global__ void plan_kernel(const uint8_t* s_c, const uint8_t* s_s, int H, int rows, int cols,
-                            int pool_n, int dense, const int32_t* valid, int order_d, PlanView pv,
-                            uint32_t* status);
+                            int pool_n, int dense, const int32_t* valid, int order_d, int ctas,
+                            PlanView pv, uint32_t* status);
 __global__ void compare_active_kernel(const uint8_t* s_c_a, const uint8_t* s_c_b, int H, int rows,
                                       int pool_n, uint32_t* status);
 
@@ -82,6 +86,8 @@ struct AttnParams {
   const uint8_t* s_s;
   const int2* items;
   const int* n_items;
+  const int* sched;       // plan att_sched: item of (wave k, CTA b) at k*gridDim.x + b
+  const int* n_waves;     // plan counts[6]
   __nv_bfloat16* out;     // [S, H*128]
   __nv_bfloat16* cache;   // update mode: [order+1, S, H*128] diff stacks (in place) or null
   int32_t* valid;         // update mode: [H, t_q] valid orders or null

@@ -100,12 +100,12 @@ __global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uin
 __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
-            PlanView pv, uint32_t* status) {
+            int ctas, PlanView pv, uint32_t* status) {
   // Attention items are ordered head-major, longest rows first within a head:
   // CTAs stride through the list together, so the K/V of the ~1-2 heads in
   // flight stay L2-resident while per-CTA work stays balanced.
   extern __shared__ int plan_smem[];
-  const int nseg = (H * (cols + 2) + 1024) * (int)sizeof(int) <= 160 * 1024 ? H : 1;
+  const int nseg = (H * (cols + 2) + 3072) * (int)sizeof(int) <= 160 * 1024 ? H : 1;
   int* hist = plan_smem;                   // [nseg][cols + 2] -> exclusive offsets
   int* scan = hist + nseg * (cols + 2);    // [1024]
   __shared__ unsigned int s_pairs[64];  // per-head pairs <= 2048 x 2048: 32-bit (native shared atomics)
@@ -251,6 +251,74 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
       pv.items[pos] = make_int2((h << 20) | i, cnt);
     }
   }
+  // pass 2b: balanced attention schedule. The item list is cut into waves of
+  // `ctas` consecutive items (head-major order keeps the K/V of the heads in
+  // flight L2-resident); within a wave the longest item goes to the CTA with
+  // the least work so far (LPT per wave). Static round-robin leaves a 3-5%
+  // spread of per-CTA work at C4 (simulated), this ~1-2%.
+  __syncthreads();
+  {
+    const int n_items = pv.counts[0];
+    const int P = ctas;  // <= 256 (checked by fo_plan): 4 threads per bin
+    int* bin_load = scan;           // [P] tiles assigned so far (scan[] is free until pass 3)
+    int* bin_of_rank = plan_smem + nseg * (cols + 2) + 1024;  // [P] (see the smem size in fo_plan)
+    int* wave_len = bin_of_rank + 1024;                         // [P] item lengths of the wave
+    for (int b = tid; b < P; b += nt) bin_load[b] = 0;
+    __syncthreads();
+    const int n_waves = ceil_div_d(n_items, P);
+    if (tid < min(P, n_items)) wave_len[tid] = pv.items[tid].y;
+    __syncthreads();
+    for (int k = 0; k < n_waves; ++k) {
+      const int base = k * P, m = min(P, n_items - base);
+      // the next wave's lengths are loaded while this one is ranked
+      const int nbase = base + P;
+      const int next_len = (tid < min(P, n_items - nbase)) ? pv.items[nbase + tid].y : 0;
+      // ranks are counted by 4 threads per element (quarter ranges, shuffle sum)
+      const int e = tid >> 2, qq = tid & 3, span = (P + 3) >> 2;
+      const int lo4 = qq * span, hi4 = min(P, lo4 + span);
+      int my_rank = 0;
+      if (e < P) {  // rank of bin e by (load, index)
+        const int my_load = bin_load[e];
+#pragma unroll 8
+        for (int b = lo4; b < hi4; ++b) {
+          const int l = bin_load[b];
+          my_rank += (l < my_load) || (l == my_load && b < e);
+        }
+      }
+      my_rank += __shfl_xor_sync(0xffffffffu, my_rank, 1);
+      my_rank += __shfl_xor_sync(0xffffffffu, my_rank, 2);
+      __syncthreads();
+      if (e < P && qq == 0) bin_of_rank[my_rank] = e;
+      __syncthreads();
+      int r = 0;
+      if (e < m) {  // rank of item e by (length desc, index)
+        const int len = wave_len[e];
+        const int hi_u = min(m, hi4);
+#pragma unroll 8
+        for (int u = lo4; u < hi_u; ++u) {
+          const int lu = wave_len[u];
+          r += (lu > len) || (lu == len && u < e);
+        }
+      }
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      if (qq == 0) {
+        if (e < m) {
+          const int b = bin_of_rank[r];
+          pv.att_sched[base + b] = base + e;
+          bin_load[b] += wave_len[e];
+        } else if (e < P) {
+          // bins ranked past the wave's items get nothing this wave (last wave only)
+          pv.att_sched[base + bin_of_rank[e]] = -1;
+        }
+      }
+      __syncthreads();
+      if (tid < min(P, n_items - nbase)) wave_len[tid] = next_len;
+      __syncthreads();
+    }
+    if (tid == 0) pv.counts[6] = n_waves;
+  }
+  __syncthreads();
   // pass 3: GEMM-Q tile list in (block, head) order: compaction via block scan
   const int per = ceil_div_d(total, nt);
   const int lo = min(total, tid * per), hi = min(total, lo + per);
