@@ -147,11 +147,13 @@ def _rms_rope_ref(y, w, pos):
 
 
 @pytest.mark.parametrize("phase", ["update", "dispatch"])
-def test_gemm_q(phase):
+@pytest.mark.parametrize("seq,dm,heads", [(384, 256, 3), (700, 192, 4), (1280, 384, 8)])
+def test_gemm_q(phase, seq, dm, heads):
+    """Odd heads (1-CTA dense path), even heads (CTA-pair dense path), a ragged
+    last block and d_model not a multiple of 128."""
     m = fo()
     torch.manual_seed(2)
-    seq, dm, heads = 384, 256, 3
-    t = seq // T
+    t = -(-seq // T)
     rng = np.random.default_rng(3)
     x = torch.randn(seq, dm, device="cuda").bfloat16()
     w_q = torch.randn(heads, dm, T, device="cuda") * dm ** -0.5
@@ -175,11 +177,13 @@ def test_gemm_q(phase):
 
 
 @pytest.mark.parametrize("order", [0, 1])
-def test_gemm_o_update_dispatch(order):
+@pytest.mark.parametrize("seq,dm", [(384, 256), (640, 384), (300, 640)])
+def test_gemm_o_update_dispatch(order, seq, dm):
+    """d_model 384 / 640 end on a 128-wide dispatch tile; 300 is a ragged block."""
     m = fo()
     torch.manual_seed(4)
-    seq, dm, heads, interval = 384, 256, 4, 4
-    t = seq // T
+    heads, interval = 4, 4
+    t = -(-seq // T)
     rng = np.random.default_rng(5)
     w_out = torch.randn(heads, T, dm, device="cuda") * T ** -0.5
     fc = m.FeatureCache(heads, t, order, seq=seq)
