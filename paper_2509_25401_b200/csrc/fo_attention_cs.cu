@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       if (w < 0) break;
       const int2 it = p.items[w];
       const int h = it.x >> 20, i = it.x & 0xFFFFF;
-      mbar_wait(&bars->q_empty, (qi & 1) ^ 1, p.status);
+      mbar_wait_small(&bars->q_empty, (qi & 1) ^ 1, p.status);
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
         tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, i * kTile);
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         while (m) {
           const int jj = base + __ffs(m) - 1;
           m &= m - 1;
-          mbar_wait(&bars->k_empty[kst], kph ^ 1, p.status);
+          mbar_wait_small(&bars->k_empty[kst], kph ^ 1, p.status);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->k_full[kst], TILE_BYTES);
             uint8_t* dk = sK + kst * TILE_BYTES;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             kst = 0;
             kph ^= 1;
           }
-          mbar_wait(&bars->v_empty[vst], vph ^ 1, p.status);
+          mbar_wait_small(&bars->v_empty[vst], vph ^ 1, p.status);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
             uint8_t* dv = sV + vst * V_STAGE_BYTES;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       const uint64_t kdesc0 = make_sdesc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t vdesc0 = make_sdesc_sw128(smem_u32(sV), HALF_BYTES, 1024);
       auto issue_qk = [&]() {
-        mbar_wait(&bars->k_full[kst], kph, p.status);
+        mbar_wait_small(&bars->k_full[kst], kph, p.status);
         tc_fence_after();
         const uint32_t sb = qk_cnt & 1;
         const uint32_t d = tbase + TM_S0 + sb * 128;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         const int w = p.sched[k * gridDim.x + blockIdx.x];
         if (w < 0) break;
         const int n = p.items[w].y;
-        mbar_wait(&bars->q_full, qi & 1, p.status);
+        mbar_wait_small(&bars->q_full, qi & 1, p.status);
         tc_fence_after();
         issue_qk();
         if (n == 1) commit_q_empty();
@@ -268,9 +268,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             issue_qk();
             if (j + 2 == n) commit_q_empty();
           }
-          mbar_wait(&bars->p_full, pv_cnt & 1, p.status);
-          if (j == 0 && qi > 0) mbar_wait(&bars->o_free, (qi - 1) & 1, p.status);
-          mbar_wait(&bars->v_full[vst], vph, p.status);
+          mbar_wait_small(&bars->p_full, pv_cnt & 1, p.status);
+          if (j == 0 && qi > 0) mbar_wait_small(&bars->o_free, (qi - 1) & 1, p.status);
+          mbar_wait_small(&bars->v_full[vst], vph, p.status);
           tc_fence_after();
           const uint32_t a_t = FO_CS_NOXCHG ? tbase + TM_P0 + (pv_cnt & 1) * 64
                                             : tbase + TM_S0 + (pv_cnt & 1) * 128;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       float2 l2 = make_float2(0.f, 0.f);
       for (int j = 0; j < n; ++j) {
         const uint32_t sb = qk_seen & 1;
-        mbar_wait(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
+        mbar_wait_small(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
         tc_fence_after();
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
         const bool mask_tail = tail && (j == n - 1);
@@ -467,11 +467,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tmem_st_wait();
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)
-          mbar_wait(&bars->o_done, (o_base + j - 1) & 1, p.status);
+          mbar_wait_small(&bars->o_done, (o_base + j - 1) & 1, p.status);
           tc_fence_after();
           const uint32_t oa = tbase + lane_off + TM_O + col0;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {  // this half of O
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {  // this half of O (rare path: kept compact)
             uint32_t o[32];
             tmem_ld32(oa + c * 32, o);
             tmem_ld_wait();
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (lane == 0) mbar_arrive(&bars->p_full);
       }
       // ---------------- epilogue: this half of O / l -> bf16 -> HBM (+ cache push)
-      mbar_wait(&bars->o_last, qi & 1, p.status);
+      mbar_wait_small(&bars->o_last, qi & 1, p.status);
       o_base += n;
       tc_fence_after();
       float l_row;

@@ -199,6 +199,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32
     }
   }
 }
+// Same, with the slow path out of line: each wait site stays a try_wait and a
+// branch. For the attention kernel, whose softmax loop is sensitive to its code
+// size (the GEMMs wait often and are faster with the inline loop).
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity, uint32_t* status) {
+  long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > 8000000000LL) {
+      raise_status(status, ST_TIMEOUT);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait_small(uint64_t* bar, uint32_t parity,
+                                                uint32_t* status = nullptr) {
+  if (mbar_try_wait(bar, parity)) return;
+  mbar_wait_slow(bar, parity, status);
+}
 
 // ---------------------------------------------------------------------------
 // TMA
