@@ -47,26 +47,6 @@
 #define FO_CS_KST 2
 #endif
 #endif
-// 1: no max exchange between the partner warps. Each warp reads the whole S row
-// (its own 64 columns are kept, the partner's are folded into the max only), so
-// both derive the same running max independently, and P goes to its own TMEM
-// buffer (columns 128-255) instead of over S, so no warp can clobber S the
-// partner has not read yet. Removes the per-tile shared-memory exchange and
-// the named barrier that kept the partners in lockstep.
-// timing experiment only (wrong results): drop the fp32 row-sum adds
-#ifndef FO_CS_NOSUM_TEST
-#define FO_CS_NOSUM_TEST 0
-#endif
-// 1 (default): one copy of the unrolled exp loop. The masked last key block
-// goes through it too (its -inf scores come out as 2^-127, not 0, far below the
-// bf16 resolution of any row sum). A/B: 1.7% faster; the softmax loop's code size
-// matters (variants that grew it were slower for no other visible reason).
-#ifndef FO_CS_ONE_EXP_LOOP
-#define FO_CS_ONE_EXP_LOOP 1
-#endif
-#ifndef FO_CS_NOXCHG
-#define FO_CS_NOXCHG 0
-#endif
 
 namespace fo {
 namespace attn_cs {
@@ -81,8 +61,6 @@ constexpr int SMEM_TILE_BYTES = TILE_BYTES * (1 + KST) + V_STAGE_BYTES * VST;
 constexpr int NTHREADS = 384;
 constexpr int SOFTMAX_THREADS = 256;
 constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
-constexpr uint32_t TM_P0 = 128;  // FO_CS_NOXCHG: P buffers (64 columns each) at 128 / 192
-static_assert(!(FO_CS_NOXCHG && FO_CS_TC_ROWSUM), "the P buffers overlap the row-sum columns");
 constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (B operand of the row-sum MMA)
 
 struct Bars {
@@ -272,8 +250,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (j == 0 && qi > 0) mbar_wait_small(&bars->o_free, (qi - 1) & 1, p.status);
           mbar_wait_small(&bars->v_full[vst], vph, p.status);
           tc_fence_after();
-          const uint32_t a_t = FO_CS_NOXCHG ? tbase + TM_P0 + (pv_cnt & 1) * 64
-                                            : tbase + TM_S0 + (pv_cnt & 1) * 128;
+          const uint32_t a_t = tbase + TM_S0 + (pv_cnt & 1) * 128;
           const uint64_t vdesc = vdesc0 + (uint64_t)((vst * V_STAGE_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
@@ -332,37 +309,6 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tc_fence_after();
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
         const bool mask_tail = tail && (j == n - 1);
-#if FO_CS_NOXCHG
-        float mo;  // max of the partner's columns, read here rather than exchanged
-        {
-          uint32_t w[2][32];
-          tmem_ld32(sa + (col0 ^ 64), w[0]);
-          tmem_ld32(sa + (col0 ^ 64) + 32, w[1]);
-          tmem_ld_wait();
-          reg_fence_cs(w[0]);
-          reg_fence_cs(w[1]);
-          const int colp = col0 ^ 64;
-          float pv[64];
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int k = 0; k < 32; ++k) pv[c * 32 + k] = __uint_as_float(w[c][k]);
-          if (mask_tail) {
-#pragma unroll
-            for (int k = 0; k < 64; ++k)
-              if (colp + k >= last_valid) pv[k] = -INFINITY;
-          }
-          float pc[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float a = fmax3f(pv[16 * c], pv[16 * c + 1], pv[16 * c + 2]);
-#pragma unroll
-            for (int k = 3; k < 15; k += 2) a = fmax3f(a, pv[16 * c + k], pv[16 * c + k + 1]);
-            pc[c] = fmaxf(a, pv[16 * c + 15]);
-          }
-          mo = fmaxf(fmax3f(pc[0], pc[1], pc[2]), pc[3]);
-        }
-#endif
         uint32_t u[2][32];
         tmem_ld32(sa + col0, u[0]);
         tmem_ld32(sa + col0 + 32, u[1]);
@@ -389,16 +335,12 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           mc[c] = fmaxf(a, sv[16 * c + 15]);
         }
         const float mh = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
-#if FO_CS_NOXCHG
-        (void)xmax_u32;
-#else
         const uint32_t xa = xmax_u32 + (((qk_seen & 1) * 2) * 128 + r) * 4;
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(xa + half * 512), "f"(mh) : "memory");
         // both partners have read their S halves before either overwrites S with P
         named_bar_sync(pair_bar, 64);
         float mo;
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(mo) : "r"(xa + (half ^ 1) * 512) : "memory");
-#endif
         ++qk_seen;
         const float m_tile = fmaxf(mh, mo) * p.scale_log2;
         bool need = false;
@@ -417,9 +359,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         l2.y *= corr;
         const float2 nm2 = make_float2(-m_new, -m_new);
         uint32_t pk[32];
-#if FO_CS_ONE_EXP_LOOP
-        // one copy of the exp loop (the hot loop's code size matters): masked tail
-        // columns are -inf, which the polynomial clamps to 2^-127 instead of 0
+        // one copy of the exp loop (the softmax loop is sensitive to its code size;
+        // a separate MUFU-only copy for the masked tail tile cost 1.7%): masked
+        // tail columns are -inf, which the polynomial clamps to 2^-127 instead of 0
         (void)mask_tail;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
@@ -431,39 +373,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             e.x = fast_exp2(x.x);
             e.y = fast_exp2(x.y);
           }
-          if (!FO_CS_TC_ROWSUM && !FO_CS_NOSUM_TEST) l2 = fadd2(l2, e);
+          if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
           pk[q] = pack_bf16x2(e.x, e.y);
         }
-#else
-        if (!mask_tail) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
-            float2 e;
-            if ((q & 7) < FO_CS_POLY_OF_8) {
-              e = exp2_poly2(x);
-            } else {
-              e.x = fast_exp2(x.x);
-              e.y = fast_exp2(x.y);
-            }
-            if (!FO_CS_TC_ROWSUM && !FO_CS_NOSUM_TEST) l2 = fadd2(l2, e);
-            pk[q] = pack_bf16x2(e.x, e.y);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
-            const float2 e = make_float2(fast_exp2(x.x), fast_exp2(x.y));  // exact zeros when masked
-            if (!FO_CS_TC_ROWSUM && !FO_CS_NOSUM_TEST) l2 = fadd2(l2, e);
-            pk[q] = pack_bf16x2(e.x, e.y);
-          }
-        }
-#endif
-#if FO_CS_NOXCHG
-        tmem_st32(tbase + lane_off + TM_P0 + sb * 64 + half * 32, pk);
-#else
         tmem_st32(sa + half * 32, pk);
-#endif
         tmem_st_wait();
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)
