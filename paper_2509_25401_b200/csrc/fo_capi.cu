@@ -192,8 +192,11 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
+  // heads (2p, 2p+1) active together go to the CTA-pair GEMM-Q (block index < 4096)
+  const int gq_pair_heads = !dense && heads % 2 == 0 && rows < 4096 && gemm_2sm_enabled();
   plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
-                                                       valid, order_d, num_sms(), pv, status);
+                                                       valid, order_d, num_sms(), gq_pair_heads, pv,
+                                                       status);
   return check_launch("plan");
 }
 
@@ -362,10 +365,14 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
     p.gq_cjobs = pv.gq_cjobs;
     p.gq_cjobs2 = pv.gq_cjobs2;
     p.n_gqc = pv.counts + 5;
+    p.gq2_jobs = pv.gq2_jobs;
+    p.n_gq2 = pv.counts + 7;
   } else {
     p.gq_pairs = nullptr;
     p.gq_cjobs = nullptr;
     p.gq_cjobs2 = nullptr;
+    p.gq2_jobs = nullptr;
+    p.n_gq2 = nullptr;
     p.n_gqc = nullptr;
   }
   p.norm_w = norm_w;
@@ -373,13 +380,16 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   p.rope_sin = rope_sin;
   p.eps = eps;
   p.q = static_cast<__nv_bfloat16*>(q_out);
-  if (dense && heads % 2 == 0 && gemm_2sm_enabled()) {
+  // CTA pairs: every tile of the dense phase; in the sparse phase the blocks
+  // where both heads of a pair (2p, 2p+1) are active (the plan's gq2 jobs, same
+  // rule as fo_plan), then the remaining tiles on the 1-CTA kernel
+  const bool pairs = heads % 2 == 0 && gemm_2sm_enabled() && (dense || t_q < 4096);
+  if (pairs) {
     CUtensorMap xm2;  // full 128-row x tiles (no multicast on the CTA-pair path)
     if ((rc = make_map(&xm2, x, seq, d_model, 128, "x"))) return rc;
     launch_gemm_q2(xm2, wm, p, (cudaStream_t)stream);
-  } else {
-    launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
   }
+  if (!(pairs && dense)) launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
   return check_launch("gemm_q");
 }
 

@@ -477,14 +477,26 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   const uint32_t tbase = bars->tmem_base;
   const int nph = p.H >> 1;                    // head pairs
   const int nbp = (p.t_q + 1) >> 1;            // block pairs
-  const int n_cjobs = nbp * nph;
+  const int n_cjobs = p.dense ? nbp * nph : *p.n_gq2;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int nkb = p.dm / BK;
-  auto job = [&](int c, int& i, int& h1, int& h2) {  // block-pair-major
-    const int bp = c / nph;
-    i = 2 * bp + rank;
-    h1 = 2 * (c - bp * nph);
+  // job -> this CTA's block i and heads (h1, h2); false: no block for this CTA
+  // (a sparse job with one block: the CTA loads zero rows past the end and
+  // skips its epilogue)
+  auto job = [&](int c, int& i, int& h1, int& h2) -> bool {
+    if (p.dense) {  // block-pair-major
+      const int bp = c / nph;
+      i = 2 * bp + rank;
+      h1 = 2 * (c - bp * nph);
+      h2 = h1 + 1;
+      return true;
+    }
+    const int code = p.gq2_jobs[c];
+    const int i0 = code & 0xFFF, i1 = ((code >> 12) & 0xFFF) - 1;
+    h1 = 2 * (code >> 24);
     h2 = h1 + 1;
+    i = rank ? (i1 >= 0 ? i1 : p.t_q) : i0;
+    return rank == 0 || i1 >= 0;
   };
 
   if (warp == 0) {
@@ -493,7 +505,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     Ring<Q2_STAGES> rg;
     for (int c = cid; c < n_cjobs; c += ncl) {
       int i, h1, h2;
-      job(c, i, h1, h2);
+      job(c, i, h1, h2);  // a missing block loads zero rows (coordinates past the end)
       const int hh = rank ? h2 : h1;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
@@ -543,15 +555,19 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl, ++t) {
       int i, h1, h2;
-      job(c, i, h1, h2);
+      const bool mine = job(c, i, h1, h2);
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, [&]() {
+      auto release = [&]() {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&bars->tempty[acc], 0);
-      });
+      };
+      if (mine)
+        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, release);
+      else
+        release();
     }
   }
   tc_fence_before();

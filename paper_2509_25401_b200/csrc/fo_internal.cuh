@@ -11,7 +11,8 @@ struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
                               // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
                               // [4] GEMM-Q head-pair jobs, [5] GEMM-Q cluster jobs,
-                              // [6] attention waves of the balanced schedule
+                              // [6] attention waves of the balanced schedule,
+                              // [7] GEMM-Q CTA-pair jobs
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
   int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
                               // the cached tiles in the same order from index counts[1]
@@ -23,6 +24,8 @@ struct PlanView {
   int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: rank 0's job index
   int* gq_cjobs2;             // [H*rows] rank 1's job index (-1: none); same block = shared x
   int* att_sched;             // [H*rows + 1024] attention item of (wave k, CTA b) at k*P + b, -1 none
+  int* gq2_jobs;              // [H*rows/2 + 64] GEMM-Q CTA-pair jobs: blocks i0, i1 x heads (2p, 2p+1)
+                              // both active; i0 | (i1 + 1) << 12 | p << 24 (i1 = -1: one block)
 };
 
 __host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
@@ -48,6 +51,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
   size_t o_gqc = take((size_t)H * rows * sizeof(int));
   size_t o_gqc2 = take((size_t)H * rows * sizeof(int));
   size_t o_sched = take(((size_t)H * rows + 1024) * sizeof(int));
+  size_t o_gq2 = take(2 * ((size_t)H * rows / 2 + 64) * sizeof(int));  // + sort scratch
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -59,6 +63,7 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->gq_cjobs = reinterpret_cast<int*>(base + o_gqc);
     pv->gq_cjobs2 = reinterpret_cast<int*>(base + o_gqc2);
     pv->att_sched = reinterpret_cast<int*>(base + o_sched);
+    pv->gq2_jobs = reinterpret_cast<int*>(base + o_gq2);
   }
   return off;
 }
@@ -70,7 +75,7 @@ __global__ void decode_symbols_kernel(const uint8_t* s_c, const uint8_t* s_s, in
                                       int cols, int pool_n, uint8_t* active, uint8_t* pair_bits);
 __global__ void plan_kernel(const uint8_t* s_c, const uint8_t* s_s, int H, int rows, int cols,
                             int pool_n, int dense, const int32_t* valid, int order_d, int ctas,
-                            PlanView pv, uint32_t* status);
+                            int gq_pair_heads, PlanView pv, uint32_t* status);
 __global__ void compare_active_kernel(const uint8_t* s_c_a, const uint8_t* s_c_b, int H, int rows,
                                       int pool_n, uint32_t* status);
 
@@ -187,6 +192,8 @@ struct GemmQParams {
   const int* gq_pairs;  // plan head-pair jobs (sparse phase)
   const int* gq_cjobs;  // plan cluster jobs over gq_pairs (sparse phase): rank 0's job
   const int* gq_cjobs2;  // rank 1's job (-1: none)
+  const int* gq2_jobs;   // CTA-pair jobs (sparse phase on gemm_q2_kernel)
+  const int* n_gq2;      // their count
   const int* n_gqc;     // their count
   const float* norm_w;  // [H, 128]
   const float* rope_cos;  // [S, 64]

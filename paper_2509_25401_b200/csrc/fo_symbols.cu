@@ -100,7 +100,7 @@ __global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uin
 __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
-            int ctas, PlanView pv, uint32_t* status) {
+            int ctas, int gq_pair_heads, PlanView pv, uint32_t* status) {
   // Attention items are ordered head-major, longest rows first within a head:
   // CTAs stride through the list together, so the K/V of the ~1-2 heads in
   // flight stay L2-resident while per-CTA work stays balanced.
@@ -350,14 +350,37 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     pv.counts[2] = 0;  // fused-forecast cursor and CTA count (attention, materialize mode)
     pv.counts[3] = 0;
   }
-  // pass 4: GEMM-Q head-pair jobs. Block i's active heads are paired in order
-  // (an odd one out runs alone), so every job is one N=256 (or N=128) tile and
-  // no skipped tile is ever computed. Jobs are block-major.
+  // pass 4: GEMM-Q head-pair jobs. With gq_pair_heads, heads (2p, 2p+1) active
+  // together in a block go to the CTA-pair kernel (pass 5); the rest here.
+  // Block i's remaining active heads are paired in order (an odd one out runs
+  // alone), so every job is one N=256 (or N=128) tile and no skipped tile is
+  // ever computed. Jobs are block-major.
   __syncthreads();  // pass 3 read scan[]; hmask (pass 1) is visible block-wide
+  // the pair path pays for itself only when it covers most of the work
+  // (measured: +3% at 75% coverage, slower at 50%): two launches and two tails
+  __shared__ int s_pair_tiles;
+  if (tid == 0) s_pair_tiles = 0;
+  __syncthreads();
+  if (gq_pair_heads) {
+    int c = 0;
+    for (int i = tid; i < rows; i += nt) {
+      const unsigned long long m = pv.hmask[i];
+      c += 2 * __popcll(m & (m >> 1) & 0x5555555555555555ull);
+    }
+    atomicAdd(&s_pair_tiles, c);
+  }
+  __syncthreads();
+  const bool use_pairs = gq_pair_heads && (long long)s_pair_tiles * 10 >= (long long)n_active * 7;
+  auto rest_mask = [&](int i) -> unsigned long long {
+    const unsigned long long m = pv.hmask[i];
+    if (!use_pairs) return m;
+    const unsigned long long both = m & (m >> 1) & 0x5555555555555555ull;  // bit 2p: pair p
+    return m & ~(both | (both << 1));
+  };
   const int per_b = ceil_div_d(rows, nt);
   const int blo = min(rows, tid * per_b), bhi = min(rows, blo + per_b);
   int nloc = 0;
-  for (int i = blo; i < bhi; ++i) nloc += (__popcll(pv.hmask[i]) + 1) >> 1;
+  for (int i = blo; i < bhi; ++i) nloc += (__popcll(rest_mask(i)) + 1) >> 1;
   scan[tid] = nloc;
   __syncthreads();
   for (int off = 1; off < nt; off <<= 1) {
@@ -374,7 +397,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   // odd jobs paired across blocks (each CTA loads its own x tile)
   int floc = 0, sloc = 0;
   for (int i = blo; i < bhi; ++i) {
-    const int nj = (__popcll(pv.hmask[i]) + 1) / 2;
+    const int nj = (__popcll(rest_mask(i)) + 1) / 2;
     floc += nj / 2;
     sloc += nj & 1;
   }
@@ -400,7 +423,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   int js = scan[tid] - sloc;
   const int n_single = scan[nt - 1];
   for (int i = blo; i < bhi; ++i) {
-    const int nj = (__popcll(pv.hmask[i]) + 1) / 2;
+    const int nj = (__popcll(rest_mask(i)) + 1) / 2;
     for (int k = 0; k + 1 < nj; k += 2) {
       pv.gq_cjobs[jf] = jp + k;
       pv.gq_cjobs2[jf++] = jp + k + 1;
@@ -413,7 +436,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
         pv.gq_cjobs[slot] = jp + nj - 1;
       ++js;
     }
-    unsigned long long m = pv.hmask[i];
+    unsigned long long m = rest_mask(i);
     while (m) {
       const int h1 = __ffsll(m) - 1;
       m &= m - 1;
@@ -429,6 +452,68 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     pv.counts[4] = n_jobs_q;
     pv.counts[5] = n_full + (n_single + 1) / 2;
     if (n_single & 1) pv.gq_cjobs2[n_full + n_single / 2] = -1;  // a lone job: rank 1 idles
+  }
+  // pass 5: CTA-pair GEMM-Q jobs: for head pair p, the blocks where both heads
+  // are active, two blocks per job (one per CTA of the pair); then ordered by
+  // first block (counting sort) so the jobs in flight share x tiles in L2
+  if (use_pairs) {
+    __syncthreads();  // scan[] of pass 4 is read
+    const int npair = H >> 1;
+    int* pcount = scan;  // [npair] jobs per pair, then their offsets
+    if (tid < npair) {
+      int c = 0;
+#pragma unroll 8
+      for (int i = 0; i < rows; ++i) c += (int)((pv.hmask[i] >> (2 * tid)) & 3ull) == 3;
+      pcount[tid] = (c + 1) >> 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int q = 0; q < npair; ++q) {
+        const int n = pcount[q];
+        pcount[q] = run;
+        run += n;
+      }
+      pv.counts[7] = run;
+    }
+    __syncthreads();
+    int* tmp = pv.gq2_jobs + (H * rows / 2 + 64);  // unsorted jobs
+    if (tid < npair) {
+      int pos = pcount[tid], pending = -1;
+#pragma unroll 8
+      for (int i = 0; i < rows; ++i) {
+        if ((int)((pv.hmask[i] >> (2 * tid)) & 3ull) != 3) continue;
+        if (pending < 0) {
+          pending = i;
+        } else {
+          tmp[pos++] = pending | ((i + 1) << 12) | (tid << 24);
+          pending = -1;
+        }
+      }
+      if (pending >= 0) tmp[pos++] = pending | (tid << 24);
+    }
+    __syncthreads();
+    const int n2 = pv.counts[7];
+    int* bcnt = hist;  // [rows] jobs per first block (hist is free after pass 2)
+    for (int i = tid; i < rows; i += nt) bcnt[i] = 0;
+    __syncthreads();
+    for (int e = tid; e < n2; e += nt) atomicAdd(&bcnt[tmp[e] & 0xFFF], 1);
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int i = 0; i < rows; ++i) {
+        const int n = bcnt[i];
+        bcnt[i] = run;
+        run += n;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < n2; e += nt) {
+      const int code = tmp[e];
+      pv.gq2_jobs[atomicAdd(&bcnt[code & 0xFFF], 1)] = code;
+    }
+  } else if (tid == 0) {
+    pv.counts[7] = 0;
   }
 }
 
