@@ -58,8 +58,17 @@ constexpr int TILE_BYTES = kTile * kTile * 2;  // 32 KB bf16 tile
 constexpr int HALF_BYTES = TILE_BYTES / 2;     // 128 rows x 64 cols, 128B-swizzled
 constexpr int V_STAGE_BYTES = FO_CS_ONESCOL ? TILE_BYTES + HALF_BYTES : TILE_BYTES;
 constexpr int SMEM_TILE_BYTES = TILE_BYTES * (1 + KST) + V_STAGE_BYTES * VST;
-constexpr int NTHREADS = 384;
-constexpr int SOFTMAX_THREADS = 256;
+// softmax warps per lane quarter (each takes 128/SPLIT key columns of its rows)
+#ifndef FO_CS_SPLIT
+#define FO_CS_SPLIT 2
+#endif
+constexpr int SPLIT = FO_CS_SPLIT;
+constexpr int NCOL = kTile / SPLIT;  // key columns per softmax warp
+constexpr int NCH = NCOL / 32;       // 32-column TMEM chunks per softmax warp
+static_assert(SPLIT == 2 || SPLIT == 4, "column split of 2 or 4 warps per lane quarter");
+static_assert(SPLIT == 2 || FO_CS_TC_ROWSUM, "a 4-way split needs the row sums in TMEM");
+constexpr int SOFTMAX_THREADS = 128 * SPLIT;
+constexpr int NTHREADS = 128 + SOFTMAX_THREADS;
 constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
 constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (B operand of the row-sum MMA)
 
@@ -70,7 +79,7 @@ struct Bars {
   uint64_t s_full[2];
   uint64_t p_full, o_done, o_last, o_free;
   uint32_t tmem_base;
-  float xmax[2][2][128];  // [tile parity][column half][row]: half-row maxima
+  float xmax[2][SPLIT][128];  // [tile parity][column group][row]: partial row maxima
   float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
   int fc_tile;            // fused forecast: the tile the softmax warps take next
 };
@@ -278,16 +287,16 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // ------------------------------------------------- softmax + epilogue (half rows)
-    const int half = (warp >= 8) ? 1 : 0;  // key columns [64*half, 64*half + 64)
+    // ------------------------------------------------- softmax + epilogue (column groups)
+    const int half = (warp - 4) >> 2;  // column group: key columns [NCOL*half, NCOL*half + NCOL)
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const int last_valid = p.S - (p.t_kv - 1) * kTile;  // valid key columns of the last block
-    const int col0 = half * 64;
+    const int col0 = half * NCOL;
     const size_t HD = (size_t)p.H * kTile;
     const size_t stack_stride = (size_t)p.S * HD;
-    const int pair_bar = 1 + q4;  // named barrier of warps (q4 + 4, q4 + 8)
+    const int pair_bar = 1 + q4;  // named barrier of the SPLIT warps of lane quarter q4
     const uint32_t xmax_u32 = smem_u32(&bars->xmax[0][0][0]);
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t qk_seen = 0, o_base = 0;
@@ -309,38 +318,46 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tc_fence_after();
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
         const bool mask_tail = tail && (j == n - 1);
-        uint32_t u[2][32];
-        tmem_ld32(sa + col0, u[0]);
-        tmem_ld32(sa + col0 + 32, u[1]);
-        tmem_ld_wait();
-        reg_fence_cs(u[0]);
-        reg_fence_cs(u[1]);
-        float sv[64];
+        uint32_t u[NCH][32];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < NCH; ++c) tmem_ld32(sa + col0 + 32 * c, u[c]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) reg_fence_cs(u[c]);
+        float sv[NCOL];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 32; ++k) sv[c * 32 + k] = __uint_as_float(u[c][k]);
         if (mask_tail) {
 #pragma unroll
-          for (int k = 0; k < 64; ++k)
+          for (int k = 0; k < NCOL; ++k)
             if (col0 + k >= last_valid) sv[k] = -INFINITY;
         }
-        // half-row max: four FMNMX3 chains of 16, then exchange with the partner warp
-        float mc[4];
+        // partial row max: FMNMX3 chains of 16, then exchange with the partner warps
+        float mc[NCOL / 16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < NCOL / 16; ++c) {
           float a = fmax3f(sv[16 * c], sv[16 * c + 1], sv[16 * c + 2]);
 #pragma unroll
           for (int k = 3; k < 15; k += 2) a = fmax3f(a, sv[16 * c + k], sv[16 * c + k + 1]);
           mc[c] = fmaxf(a, sv[16 * c + 15]);
         }
-        const float mh = fmaxf(fmax3f(mc[0], mc[1], mc[2]), mc[3]);
-        const uint32_t xa = xmax_u32 + (((qk_seen & 1) * 2) * 128 + r) * 4;
+        float mh = mc[0];
+#pragma unroll
+        for (int c = 1; c < NCOL / 16; ++c) mh = fmaxf(mh, mc[c]);
+        const uint32_t xa = xmax_u32 + (((qk_seen & 1) * SPLIT) * 128 + r) * 4;
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(xa + half * 512), "f"(mh) : "memory");
-        // both partners have read their S halves before either overwrites S with P
-        named_bar_sync(pair_bar, 64);
-        float mo;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(mo) : "r"(xa + (half ^ 1) * 512) : "memory");
+        // all partners have read their S columns before any overwrites S with P
+        named_bar_sync(pair_bar, 32 * SPLIT);
+        float mo = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < SPLIT; ++g) {
+          if (g == half) continue;
+          float v;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xa + g * 512) : "memory");
+          mo = fmaxf(mo, v);
+        }
         ++qk_seen;
         const float m_tile = fmaxf(mh, mo) * p.scale_log2;
         bool need = false;
@@ -358,13 +375,13 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         l2.x *= corr;  // the running sum moves to the new max before this tile adds to it
         l2.y *= corr;
         const float2 nm2 = make_float2(-m_new, -m_new);
-        uint32_t pk[32];
+        uint32_t pk[NCOL / 2];
         // one copy of the exp loop (the softmax loop is sensitive to its code size;
         // a separate MUFU-only copy for the masked tail tile cost 1.7%): masked
         // tail columns are -inf, which the polynomial clamps to 2^-127 instead of 0
         (void)mask_tail;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < NCOL / 2; ++q) {
           const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
           float2 e;
           if ((q & 7) < FO_CS_POLY_OF_8) {
@@ -376,7 +393,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
           pk[q] = pack_bf16x2(e.x, e.y);
         }
+#if FO_CS_SPLIT == 2
         tmem_st32(sa + half * 32, pk);
+#else
+        tmem_st16(sa + half * 16, pk);
+#endif
         tmem_st_wait();
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)
@@ -384,7 +405,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           tc_fence_after();
           const uint32_t oa = tbase + lane_off + TM_O + col0;
 #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {  // this half of O (rare path: kept compact)
+          for (int c = 0; c < NCH; ++c) {  // this warp's columns of O (rare path: kept compact)
             uint32_t o[32];
             tmem_ld32(oa + c * 32, o);
             tmem_ld_wait();
@@ -421,7 +442,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         l_row = __uint_as_float(lsum[0]);
       } else {
         // combine the two halves' partial sums (both scaled by the same maxima)
-        bars->xsum[half][r] = l2.x + l2.y;
+        bars->xsum[half][r] = l2.x + l2.y;  // SPLIT == 2 here (static_assert above)
         named_bar_sync(pair_bar, 64);
         l_row = bars->xsum[0][r] + bars->xsum[1][r];
       }
@@ -431,7 +452,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       const int vn = min(valid_old + 1, p.order_d + 1);
       const uint32_t oa = tbase + lane_off + TM_O + col0;
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         uint32_t o[32];
         tmem_ld32(oa + c * 32, o);
         tmem_ld_wait();
