@@ -11,10 +11,10 @@
 //                      sequential column sums (policy.py:68-77)
 //   prefix selection   stable ascending order (ties -> lower index), fp64
 //                      sequential cumsum, csum <= budget (* total) (policy.py:80-121)
-// Four small launches: pool (thread per (head, block, dim)), scores (warp per
-// (head, compressed row)), cache selection (CTA per head), skip selection
-// (warp per (head, compressed row)). The compressed map of a 33K-token layer
-// is 258 x 258 per head, so all of it is a few tens of microseconds.
+// Four small launches: pool (q and k, thread per (head, block, dim pair)),
+// scores (CTA per (head, 16 compressed rows)), cache selection (CTA per head),
+// skip selection (warp per (head, compressed row)). The compressed map of a
+// 33K-token layer is 258 x 258 per head.
 #include "fo_internal.cuh"
 
 namespace fo {
@@ -23,16 +23,32 @@ namespace {
 
 constexpr int kPolWarps = 4;  // warps per CTA in the per-row kernels
 
-__global__ void pool_kernel(const __nv_bfloat16* __restrict__ x, int S, int H, int block, int rows_c,
-                            float* __restrict__ out) {  // [H, rows_c, 128]
+// thread per (tensor, block, head, dim pair): q and k in one launch, bf16x2
+// loads (a warp reads 128 contiguous bytes of a row), fp64 sums in row order.
+__global__ void pool_kernel(const __nv_bfloat16* __restrict__ xq, const __nv_bfloat16* __restrict__ xk,
+                            int S, int H, int block, int rows_c, float* __restrict__ oq,
+                            float* __restrict__ ok) {  // [H, rows_c, 128] each
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= H * rows_c * kTile) return;
-  const int d = idx % kTile, r = (idx / kTile) % rows_c, h = idx / (kTile * rows_c);
+  if (idx >= H * rows_c * (kTile / 2)) return;
+  const __nv_bfloat16* x = blockIdx.y ? xk : xq;
+  float* out = blockIdx.y ? ok : oq;
+  // heads vary fastest after the dims: consecutive warps read one token row
+  const int d = 2 * (idx % (kTile / 2)), h = (idx / (kTile / 2)) % H,
+            r = idx / ((kTile / 2) * H);
   const int s0 = r * block, s1 = min(S, s0 + block);
-  double acc = 0.0;  // np.add.reduceat: sequential from the first element
-  for (int s = s0; s < s1; ++s)
-    acc += (double)__bfloat162float(x[(size_t)s * H * kTile + (size_t)h * kTile + d]);
-  out[idx] = (float)(acc / (double)(s1 - s0));
+  const uint32_t* p =
+      reinterpret_cast<const uint32_t*>(x + (size_t)s0 * H * kTile + (size_t)h * kTile + d);
+  const size_t stride = (size_t)H * kTile / 2;
+  double a0 = 0.0, a1 = 0.0;  // np.add.reduceat: sequential from the first element
+#pragma unroll 8
+  for (int s = s0; s < s1; ++s, p += stride) {
+    const uint32_t v = __ldg(p);
+    a0 += (double)__uint_as_float(v << 16);
+    a1 += (double)__uint_as_float(v & 0xFFFF0000u);
+  }
+  const double n = (double)(s1 - s0);
+  *reinterpret_cast<float2*>(out + (size_t)(h * rows_c + r) * kTile + d) =
+      make_float2((float)(a0 / n), (float)(a1 / n));
 }
 
 __device__ double pairwise_leaf(const double* p, int n) {
@@ -67,36 +83,113 @@ __device__ double pairwise_sum<0>(const double* a, int n) {
   return pairwise_leaf(a, n);  // unreachable for n <= kPolicyMaxBlocks
 }
 
-// row_softmax of one fp32 row (length n >= 1) into out (fp32); e: fp64 scratch
-__device__ void row_softmax_serial(const float* s, int n, double* e, float* out) {
-  float mx = s[0];
-  for (int i = 1; i < n; ++i) mx = fmaxf(mx, s[i]);
-  for (int i = 0; i < n; ++i) e[i] = exp((double)s[i] - (double)mx);
-  const double sum = pairwise_sum<5>(e, n);
-  for (int i = 0; i < n; ++i) out[i] = (float)(e[i] / sum);
+// Scores + row softmax. CTA per (head, 16 compressed rows), 4 warps of 4
+// rows. The head's pooled k is staged through shared memory as fp64,
+// transposed ([d][column], 64 columns per chunk) so a lane's column reads are
+// conflict-free and every element is converted once; each lane keeps 4 rows x
+// 2 columns of fp64 accumulators, summed over d in order (the same arithmetic
+// as a per-column loop). The softmax exponentials run across the warp; lane 0
+// does numpy's pairwise sum.
+constexpr int kScWarps = 4, kScRows = 4, kScChunk = 64;
+
+size_t scores_smem_bytes(int cols) {
+  return (size_t)kTile * kScChunk * 8 + (size_t)kScWarps * kScRows * kTile * 8 +
+         (size_t)kScWarps * cols * 8 + (size_t)kScWarps * kScRows * cols * 4;
 }
 
-// warp per (head, compressed row): p_tilde[h, r, :]
-__global__ void scores_kernel(const float* __restrict__ pq, const float* __restrict__ pk, int H,
-                              int rows_c, float* __restrict__ p_tilde) {
-  extern __shared__ double pol_smem[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kPolWarps + wib;
-  if (gw >= H * rows_c) return;
+__global__ void __launch_bounds__(kScWarps * 32, 2)
+scores_kernel(const float* __restrict__ pq, const float* __restrict__ pk, int rows_c,
+              float* __restrict__ p_tilde) {
+  extern __shared__ __align__(16) unsigned char sc_smem[];
   const int cols = rows_c;
-  const int h = gw / rows_c, r = gw % rows_c;
-  double* e = pol_smem + (size_t)wib * cols * 2;
-  float* s = reinterpret_cast<float*>(e + cols);
-  const float* qr = pq + ((size_t)h * rows_c + r) * kTile;
+  double* pkT = reinterpret_cast<double*>(sc_smem);                 // [128][kScChunk]
+  double* qs = pkT + kTile * kScChunk;                              // [warp][row][128]
+  double* e = qs + kScWarps * kScRows * kTile;                      // [warp][cols]
+  float* srow = reinterpret_cast<float*>(e + kScWarps * cols);      // [warp][row][cols]
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31, h = blockIdx.y;
+  const int r0 = (blockIdx.x * kScWarps + wib) * kScRows;
+  double* qw = qs + wib * kScRows * kTile;
+  float* sw = srow + (size_t)wib * kScRows * cols;
+  double* ew = e + (size_t)wib * cols;
+  {
+    float qv[kScRows][kTile / 32];  // loads first: one L2 round trip, not sixteen
+#pragma unroll
+    for (int i = 0; i < kScRows; ++i)
+#pragma unroll
+      for (int u = 0; u < kTile / 32; ++u)
+        qv[i][u] = r0 + i < rows_c ? __ldg(&pq[((size_t)h * rows_c + r0 + i) * kTile + lane + 32 * u]) : 0.f;
+#pragma unroll
+    for (int i = 0; i < kScRows; ++i)
+#pragma unroll
+      for (int u = 0; u < kTile / 32; ++u) qw[i * kTile + lane + 32 * u] = (double)qv[i][u];
+  }
   const double rs = sqrt((double)kTile);
-  for (int c = lane; c < cols; c += 32) {
-    const float* kc = pk + ((size_t)h * cols + c) * kTile;
-    double acc = 0.0;
-    for (int d = 0; d < kTile; ++d) acc += (double)qr[d] * (double)kc[d];
-    s[c] = (float)(acc / rs);
+  const float4* pk4 = reinterpret_cast<const float4*>(pk + (size_t)h * cols * kTile);
+  const int nchunk = (cols + kScChunk - 1) / kScChunk;
+  const int csz = ((cols + nchunk - 1) / nchunk + 31) & ~31;  // balanced, multiple of 32
+  const int jn = csz >> 5;
+  // the next chunk's loads are in flight while this chunk computes
+  constexpr int kLd = kScChunk * (kTile / 4) / (kScWarps * 32);
+  float4 v[kLd];
+  auto load_chunk = [&](int c0) {
+    const int cn = min(csz, cols - c0);
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int idx = threadIdx.x + u * kScWarps * 32, c = idx % kScChunk, d4 = idx / kScChunk;
+      v[u] = c < cn ? __ldg(&pk4[(size_t)(c0 + c) * (kTile / 4) + d4]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  load_chunk(0);
+  for (int c0 = 0; c0 < cols; c0 += csz) {
+    const int cn = min(csz, cols - c0);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int idx = threadIdx.x + u * kScWarps * 32, c = idx % kScChunk, d4 = idx / kScChunk;
+      pkT[(4 * d4 + 0) * kScChunk + c] = (double)v[u].x;
+      pkT[(4 * d4 + 1) * kScChunk + c] = (double)v[u].y;
+      pkT[(4 * d4 + 2) * kScChunk + c] = (double)v[u].z;
+      pkT[(4 * d4 + 3) * kScChunk + c] = (double)v[u].w;
+    }
+    if (c0 + csz < cols) load_chunk(c0 + csz);
+    __syncthreads();
+    if (r0 >= rows_c) continue;
+    double acc[kScRows][2] = {};
+#pragma unroll 2
+    for (int d = 0; d < kTile; ++d) {
+      const double k0 = pkT[d * kScChunk + lane];
+      const double k1 = jn > 1 ? pkT[d * kScChunk + lane + 32] : 0.0;
+#pragma unroll
+      for (int i = 0; i < kScRows; ++i) {
+        const double qd = qw[i * kTile + d];
+        acc[i][0] += qd * k0;
+        acc[i][1] += qd * k1;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kScRows; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j;
+        if (r0 + i < rows_c && c < cn) sw[i * cols + c0 + c] = (float)(acc[i][j] / rs);
+      }
   }
   __syncwarp();
-  if (lane == 0) row_softmax_serial(s, cols, e, p_tilde + ((size_t)h * rows_c + r) * cols);
+  for (int i = 0; i < kScRows; ++i) {
+    if (r0 + i >= rows_c) break;
+    const float* s = sw + i * cols;
+    float mx = -INFINITY;  // max is order independent for finite scores
+    for (int c = lane; c < cols; c += 32) mx = fmaxf(mx, s[c]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int c = lane; c < cols; c += 32) ew[c] = exp((double)s[c] - (double)mx);
+    __syncwarp();
+    double sum = 0.0;
+    if (lane == 0) sum = pairwise_sum<5>(ew, cols);
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    float* out = p_tilde + ((size_t)h * rows_c + r0 + i) * cols;
+    for (int c = lane; c < cols; c += 32) out[c] = (float)(ew[c] / sum);
+    __syncwarp();
+  }
 }
 
 // Stable ascending budget prefix over v[0, n) (fp64 copies of fp32 values).
@@ -146,8 +239,7 @@ __device__ int budget_prefix(const double* v, int n, double budget, bool relativ
 // CTA per head: contribution / guidance -> compressed compute bits + degrade.
 __global__ void __launch_bounds__(256)
 cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, double tau_q,
-                    double s_q, uint8_t* __restrict__ comp_cache,  // [H, rows_c]
-                    double* __restrict__ gscratch) {               // [H, 4 * rows_c] doubles
+                    double s_q, uint8_t* __restrict__ comp_cache) {  // [H, rows_c]
   extern __shared__ double cs_smem[];
   const int h = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int cols = rows_c, V = rows_c - n_t;
@@ -158,6 +250,10 @@ cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, doub
   int* rank = reinterpret_cast<int*>(sorted + rows_c);         // [V]
   uint8_t* cut_c = reinterpret_cast<uint8_t*>(rank + rows_c);  // [V]
   uint8_t* cc = cut_c + rows_c;                                // [rows_c]
+  double* e = reinterpret_cast<double*>(                        // [V] guidance scratch
+      (reinterpret_cast<uintptr_t>(cc + rows_c) + 7) & ~uintptr_t(7));
+  float* tmp = reinterpret_cast<float*>(e + rows_c);           // [V]
+  float* acc = tmp + rows_c;                                   // [V]
   // vision_to_text_contribution: p[:n_t, n_t:].sum(axis=0), fp32 row by row
   for (int c = tid; c < V; c += nt) {
     float a = 0.f;
@@ -168,23 +264,33 @@ cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, doub
     contrib[c] = (double)a;
   }
   // text_to_vision_guidance: text column j re-softmaxed over the vision rows,
-  // then fp32 sums over j (serial: n_t is a handful of compressed blocks)
-  if (tid == 0) {
-    if (n_t > 0) {
-      double* e = gscratch + (size_t)h * 4 * rows_c;
-      float* tmp = reinterpret_cast<float*>(e + rows_c);
-      float* beta = tmp + rows_c;
-      float* acc = reinterpret_cast<float*>(e + 2 * rows_c);
-      for (int j = 0; j < n_t; ++j) {
-        for (int c = 0; c < V; ++c) tmp[c] = P[(size_t)(n_t + c) * cols + j];
-        row_softmax_serial(tmp, V, e, beta);
-        for (int c = 0; c < V; ++c) acc[c] = j ? acc[c] + beta[c] : beta[c];
-      }
-      for (int c = 0; c < V; ++c) guid[c] = (double)acc[c];
-    } else {
-      for (int c = 0; c < V; ++c) guid[c] = 0.0;
+  // then fp32 sums over j in order (exponentials across the CTA, numpy's
+  // pairwise sum on one thread)
+  __shared__ float red[32];
+  __shared__ double s_sum;
+  for (int j = 0; j < n_t; ++j) {
+    float mx = -INFINITY;
+    for (int c = tid; c < V; c += nt) {
+      tmp[c] = P[(size_t)(n_t + c) * cols + j];
+      mx = fmaxf(mx, tmp[c]);
     }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < nt / 32; ++w) mx = fmaxf(mx, red[w]);
+    for (int c = tid; c < V; c += nt) e[c] = exp((double)tmp[c] - (double)mx);
+    __syncthreads();
+    if (tid == 0) s_sum = pairwise_sum<5>(e, V);
+    __syncthreads();
+    const double sum = s_sum;
+    for (int c = tid; c < V; c += nt) {
+      const float beta = (float)(e[c] / sum);
+      acc[c] = j ? acc[c] + beta : beta;
+    }
+    __syncthreads();
   }
+  for (int c = tid; c < V; c += nt) guid[c] = n_t > 0 ? (double)acc[c] : 0.0;
   __syncthreads();
   // select_cached_blocks: both ascending prefixes within tau_q of their totals
   int cut = budget_prefix<true>(contrib, V, tau_q, true, rank, sorted, tid, nt);
@@ -268,9 +374,9 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t policy_workspace_bytes(int H, int rows_c) {
   // pooled q, k [H, rows_c, 128] fp32 | p_tilde [H, rows_c, rows_c] fp32 |
-  // compressed compute bits [H, rows_c] | guidance scratch [H, 4 rows_c] fp64
+  // compressed compute bits [H, rows_c]
   return 2 * al256((size_t)H * rows_c * kTile * 4) + al256((size_t)H * rows_c * rows_c * 4) +
-         al256((size_t)H * rows_c) + al256((size_t)H * 4 * rows_c * 8);
+         al256((size_t)H * rows_c);
 }
 
 cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k, int S, int H,
@@ -288,20 +394,21 @@ cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k
   float* pt = reinterpret_cast<float*>(w);
   w += al256((size_t)H * rows_c * rows_c * 4);
   uint8_t* cc = reinterpret_cast<uint8_t*>(w);
-  w += al256((size_t)H * rows_c);
-  double* gs = reinterpret_cast<double*>(w);
 
-  const int n_pool = H * rows_c * kTile;
-  pool_kernel<<<(n_pool + 255) / 256, 256, 0, stream>>>(q, S, H, block, rows_c, pq);
-  pool_kernel<<<(n_pool + 255) / 256, 256, 0, stream>>>(k, S, H, block, rows_c, pk);
+  const int n_pool = H * rows_c * (kTile / 2);
+  pool_kernel<<<dim3((n_pool + 255) / 256, 2), 256, 0, stream>>>(q, k, S, H, block, rows_c, pq, pk);
+  const size_t sm_sc = scores_smem_bytes(rows_c);
+  cudaFuncSetAttribute(scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc);
+  const int rows_cta = kScWarps * kScRows;
+  scores_kernel<<<dim3((rows_c + rows_cta - 1) / rows_cta, H), kScWarps * 32, sm_sc, stream>>>(
+      pq, pk, rows_c, pt);
   const int grid_rows = (H * rows_c + kPolWarps - 1) / kPolWarps;
   const size_t sm_rows = (size_t)kPolWarps * rows_c * 3 * sizeof(double);
-  cudaFuncSetAttribute(scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows);
-  scores_kernel<<<grid_rows, kPolWarps * 32, sm_rows, stream>>>(pq, pk, H, rows_c, pt);
-  const size_t sm_cache = (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2);
+  const size_t sm_cache =
+      (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2) + 8 + (size_t)rows_c * (8 + 4 + 4);
   cudaFuncSetAttribute(cache_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm_cache);
-  cache_select_kernel<<<H, 256, sm_cache, stream>>>(pt, rows_c, n_t, tau_q, s_q, cc, gs);
+  cache_select_kernel<<<H, 256, sm_cache, stream>>>(pt, rows_c, n_t, tau_q, s_q, cc);
   cudaFuncSetAttribute(skip_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows);
   skip_select_kernel<<<grid_rows, kPolWarps * 32, sm_rows, stream>>>(
       pt, cc, H, rows_c, n_t, tau_kv, guard, pool_n, t_q, cache_bits, skip_bits);

@@ -35,7 +35,7 @@ def test_plan_layout_sizes():
 
     lib = _lib.load()
     n = lib.fo_plan_workspace_bytes(24, 258)
-    offs = (ctypes.c_size_t * 6)()
+    offs = (ctypes.c_size_t * 7)()  # fo_plan_offsets writes seven offsets
     lib.fo_plan_offsets(24, 258, offs)
     assert all(o % 16 == 0 for o in offs)
     assert list(offs) == sorted(offs) and offs[-1] < n
