@@ -95,6 +95,15 @@ __device__ __forceinline__ void reg_fence_cs(uint32_t (&r)[N]) {
 }
 }  // namespace
 
+#ifdef FO_CS_TIMING  // tools/cs_timing.py: per-CTA start/end (globaltimer), SM id, tiles
+__device__ unsigned long long g_cs_timing[4 * 1024];
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     sparse_attention_cs_kernel(const __grid_constant__ CUtensorMap qm,
                                const __grid_constant__ CUtensorMap km,
@@ -145,6 +154,15 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
+#ifdef FO_CS_TIMING
+  if (threadIdx.x == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_cs_timing[4 * blockIdx.x] = global_ns();
+    g_cs_timing[4 * blockIdx.x + 2] = smid;
+    g_cs_timing[4 * blockIdx.x + 3] = 0;
+  }
+#endif
   const int n_items = *p.n_items;
   const int n_waves = *p.n_waves;  // plan schedule: CTA b's k-th item is sched[k * grid + b]
   (void)n_items;
@@ -518,6 +536,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       tc_fence_before();
       mbar_arrive(&bars->o_free);
       if (r == 0 && half == 0) {
+#ifdef FO_CS_TIMING
+        atomicAdd(&g_cs_timing[4 * blockIdx.x + 3], (unsigned long long)n);
+#endif
         if (p.pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
                                static_cast<unsigned long long>(n));
         if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
@@ -528,11 +549,21 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef FO_CS_TIMING
+  if (threadIdx.x == 0) g_cs_timing[4 * blockIdx.x + 1] = global_ns();
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
 }
+
+#ifdef FO_CS_TIMING
+extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigned long long* out,
+                                                                       int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 4 * n);
+}
+#endif
 
 void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
                          const AttnParams& p, int grid, cudaStream_t stream) {
