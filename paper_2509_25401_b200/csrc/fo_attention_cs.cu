@@ -95,8 +95,37 @@ __device__ __forceinline__ void reg_fence_cs(uint32_t (&r)[N]) {
 }
 }  // namespace
 
+// This CTA's item sequence (plan schedule: the k-th item is sched[k * grid +
+// blockIdx.x]), read ahead: the schedule entry two items ahead and the item
+// record one item ahead are loaded while the current item runs. Read at the
+// top of each item, the two dependent global loads stalled every role ~1 us
+// per item (the MMA warp's first QK, the producer's Q load).
+struct ItemCursor {
+  const int* sched;
+  const int2* items;
+  int n_waves, w1, w2;
+  int2 it1;
+  __device__ ItemCursor(const int* s, const int2* its, int nw) : sched(s), items(its), n_waves(nw) {
+    w1 = nw > 0 ? s[blockIdx.x] : -1;
+    it1 = w1 >= 0 ? its[w1] : make_int2(0, 0);
+    w2 = nw > 1 ? s[gridDim.x + blockIdx.x] : -1;
+  }
+  // item k (call with k = 0, 1, ...): false at the end of the schedule
+  __device__ __forceinline__ bool next(int k, int& w, int2& it) {
+    w = w1;
+    it = it1;
+    if (w < 0) return false;
+    w1 = w2;
+    it1 = w2 >= 0 ? items[w2] : make_int2(0, 0);
+    w2 = k + 2 < n_waves ? sched[(k + 2) * gridDim.x + blockIdx.x] : -1;
+    return true;
+  }
+  __device__ __forceinline__ int peek_w() const { return w1; }
+  __device__ __forceinline__ int2 peek_item() const { return it1; }
+};
+
 #ifdef FO_CS_TIMING  // tools/cs_timing.py: per-CTA start/end (globaltimer), SM id, tiles
-__device__ unsigned long long g_cs_timing[4 * 1024];
+__device__ unsigned long long g_cs_timing[12 * 1024];
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -158,9 +187,13 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   if (threadIdx.x == 0) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    g_cs_timing[4 * blockIdx.x] = global_ns();
-    g_cs_timing[4 * blockIdx.x + 2] = smid;
-    g_cs_timing[4 * blockIdx.x + 3] = 0;
+    g_cs_timing[12 * blockIdx.x] = global_ns();
+    g_cs_timing[12 * blockIdx.x + 2] = smid;
+    g_cs_timing[12 * blockIdx.x + 3] = 0;
+    g_cs_timing[12 * blockIdx.x + 8] = 0;
+    g_cs_timing[12 * blockIdx.x + 9] = 0;
+    g_cs_timing[12 * blockIdx.x + 10] = 0;
+    g_cs_timing[12 * blockIdx.x + 11] = 0;
   }
 #endif
   const int n_items = *p.n_items;
@@ -171,16 +204,31 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
+    ItemCursor sched_cur(p.sched, p.items, n_waves);
     for (int k = 0; k < n_waves; ++k, ++qi) {
-      const int w = p.sched[k * gridDim.x + blockIdx.x];
-      if (w < 0) break;
-      const int2 it = p.items[w];
+      int w;
+      int2 it;
+      if (!sched_cur.next(k, w, it)) break;
       const int h = it.x >> 20, i = it.x & 0xFFFFF;
+#ifdef FO_CS_TIMING
+      const unsigned long long tq0 = global_ns();
+#endif
       mbar_wait_small(&bars->q_empty, (qi & 1) ^ 1, p.status);
+#ifdef FO_CS_TIMING
+      if (lane == 0 && k > 0) g_cs_timing[12 * blockIdx.x + 8] += global_ns() - tq0;
+#endif
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
         tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, i * kTile);
         tma_load_2d(sQ + HALF_BYTES, &qm, &bars->q_full, h * kTile + 64, i * kTile);
+        // the next item's Q into L2 now: its load is only issued once this
+        // item's last QK is done, and from HBM it would stall the next item's
+        // first QK by ~1 us
+        if (sched_cur.peek_w() >= 0) {
+          const int2 itn = sched_cur.peek_item();
+          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile, (itn.x & 0xFFFFF) * kTile);
+          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile + 64, (itn.x & 0xFFFFF) * kTile);
+        }
       }
       __syncwarp();
       const uint8_t* sym = p.s_s + h * head_sym;
@@ -260,17 +308,36 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (elect_one()) tc_commit(&bars->q_empty);
         __syncwarp();
       };
+      ItemCursor sched_cur(p.sched, p.items, n_waves);
+#ifdef FO_CS_TIMING
+      unsigned long long t_pvl = 0;
+#endif
       for (int k = 0; k < n_waves; ++k, ++qi) {
-        const int w = p.sched[k * gridDim.x + blockIdx.x];
-        if (w < 0) break;
-        const int n = p.items[w].y;
+        int w;
+        int2 it;
+        if (!sched_cur.next(k, w, it)) break;
+        const int n = it.y;
         mbar_wait_small(&bars->q_full, qi & 1, p.status);
+#ifdef FO_CS_TIMING
+        if (lane == 0 && k > 0) g_cs_timing[12 * blockIdx.x + 9] += global_ns() - t_pvl;
+#endif
         tc_fence_after();
         issue_qk();
+#ifdef FO_CS_TIMING
+        if (k > 0) {
+          const unsigned long long t0 = global_ns();
+          const uint32_t c = qk_cnt - 1;
+          while (!mbar_try_wait(&bars->s_full[c & 1], (c >> 1) & 1)) {
+          }
+          if (lane == 0) g_cs_timing[12 * blockIdx.x + 11] += global_ns() - t0;
+        }
+#endif
         if (n == 1) commit_q_empty();
         for (int j = 0; j < n; ++j) {
           if (j + 1 < n) {
             issue_qk();
+#ifdef FO_CS_TIMING
+#endif
             if (j + 2 == n) commit_q_empty();
           }
           mbar_wait_small(&bars->p_full, pv_cnt & 1, p.status);
@@ -301,6 +368,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           }
           ++pv_cnt;
         }
+#ifdef FO_CS_TIMING
+        t_pvl = global_ns();
+#endif
       }
     }
     __syncwarp();
@@ -319,20 +389,42 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t qk_seen = 0, o_base = 0;
     int qi = 0;
-    for (int k = 0; k < n_waves; ++k, ++qi) {
-      const int w = p.sched[k * gridDim.x + blockIdx.x];
-      if (w < 0) break;
-      const int2 it = p.items[w];
+    ItemCursor sched_cur(p.sched, p.items, n_waves);
+    // the next item's record and cache counter are fetched before this item's
+    // epilogue stores: a global load or atomic issued behind 8 uncoalesced
+    // 16-B stores per thread waits for them to drain (~0.9 us per item)
+    auto valid_of = [&](int2 itv) {
+      return (p.cache && p.valid) ? p.valid[(size_t)(itv.x >> 20) * p.t_q + (itv.x & 0xFFFFF)] : 0;
+    };
+    int w_cur;
+    int2 it_cur;
+    bool have = sched_cur.next(0, w_cur, it_cur);
+    int valid_cur = have ? valid_of(it_cur) : 0;
+#ifdef FO_CS_TIMING
+    const bool tmr = threadIdx.x == 128;
+    unsigned long long t_mark = 0, g_a = 0, g_b = 0, g_c = 0, n_it = 0;
+#endif
+    for (int k = 0; have; ++k, ++qi) {
+      const int2 it = it_cur;
       const int h = it.x >> 20, i = it.x & 0xFFFFF, n = it.y;
       const bool tail = (last_valid < kTile) &&
                         (p.dense || decode_reduction(p.s_s + h * head_sym, p.row_stride, i,
                                                      p.t_kv - 1, p.pool_n));
-      const int valid_old = (p.cache && p.valid) ? p.valid[(size_t)h * p.t_q + i] : 0;
+      const int valid_old = valid_cur;
       float m_run = -INFINITY;
       float2 l2 = make_float2(0.f, 0.f);
       for (int j = 0; j < n; ++j) {
         const uint32_t sb = qk_seen & 1;
+#ifdef FO_CS_TIMING
+        if (tmr && j == 0 && t_mark) g_cs_timing[12 * blockIdx.x + 10] += global_ns() - t_mark;
+#endif
         mbar_wait_small(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
+#ifdef FO_CS_TIMING
+        if (tmr && j == 0 && t_mark) {
+          const unsigned long long t = global_ns();
+          g_c += t - t_mark;  // epilogue end -> first S
+        }
+#endif
         tc_fence_after();
         const uint32_t sa = tbase + lane_off + TM_S0 + sb * 128;
         const bool mask_tail = tail && (j == n - 1);
@@ -448,7 +540,18 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (lane == 0) mbar_arrive(&bars->p_full);
       }
       // ---------------- epilogue: this half of O / l -> bf16 -> HBM (+ cache push)
+#ifdef FO_CS_TIMING
+      if (tmr) t_mark = global_ns();
+#endif
       mbar_wait_small(&bars->o_last, qi & 1, p.status);
+#ifdef FO_CS_TIMING
+      if (tmr) {
+        const unsigned long long t = global_ns();
+        g_a += t - t_mark;  // last P stored -> last PV complete
+        t_mark = t;
+        ++n_it;
+      }
+#endif
       o_base += n;
       tc_fence_after();
       float l_row;
@@ -468,6 +571,21 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       const int row = i * kTile + r;
       const bool row_ok = row < p.S;
       const int vn = min(valid_old + 1, p.order_d + 1);
+      {
+        int w_n;
+        int2 it_n;
+        have = sched_cur.next(k + 1, w_n, it_n);
+        it_cur = it_n;
+        valid_cur = have ? valid_of(it_n) : 0;
+      }
+      if (r == 0 && half == 0) {
+#ifdef FO_CS_TIMING
+        atomicAdd(&g_cs_timing[12 * blockIdx.x + 3], (unsigned long long)n);
+#endif
+        if (p.pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
+                               static_cast<unsigned long long>(n));
+        if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
+      }
       const uint32_t oa = tbase + lane_off + TM_O + col0;
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c) {
@@ -480,16 +598,16 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         for (int k = 0; k < 32; ++k) of[k] = __uint_as_float(o[k]) * inv_l;
         if (row_ok) {
           const size_t off = (size_t)row * HD + (size_t)h * kTile + col0 + c * 32;
-          uint4* dst = reinterpret_cast<uint4*>(p.out + off);
+          uint4 pk4[4];
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
-            uint4 pkv;
-            pkv.x = pack_bf16x2(of[v4 * 8 + 0], of[v4 * 8 + 1]);
-            pkv.y = pack_bf16x2(of[v4 * 8 + 2], of[v4 * 8 + 3]);
-            pkv.z = pack_bf16x2(of[v4 * 8 + 4], of[v4 * 8 + 5]);
-            pkv.w = pack_bf16x2(of[v4 * 8 + 6], of[v4 * 8 + 7]);
-            dst[v4] = pkv;
+            pk4[v4].x = pack_bf16x2(of[v4 * 8 + 0], of[v4 * 8 + 1]);
+            pk4[v4].y = pack_bf16x2(of[v4 * 8 + 2], of[v4 * 8 + 3]);
+            pk4[v4].z = pack_bf16x2(of[v4 * 8 + 4], of[v4 * 8 + 5]);
+            pk4[v4].w = pack_bf16x2(of[v4 * 8 + 6], of[v4 * 8 + 7]);
           }
+          st_global_256(p.out + off, pk4[0], pk4[1]);
+          st_global_256(p.out + off + 16, pk4[2], pk4[3]);
           if (p.cache) {
             // backward-difference push: new[0]=o, new[d]=new[d-1]-old[d-1] for d<vn, else 0
             float cur[32];
@@ -535,22 +653,29 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&bars->o_free);
-      if (r == 0 && half == 0) {
 #ifdef FO_CS_TIMING
-        atomicAdd(&g_cs_timing[4 * blockIdx.x + 3], (unsigned long long)n);
-#endif
-        if (p.pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
-                               static_cast<unsigned long long>(n));
-        if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
+      if (tmr) {
+        const unsigned long long t = global_ns();
+        g_b += t - t_mark;  // epilogue
+        t_mark = t;
       }
+#endif
     }
+#ifdef FO_CS_TIMING
+    if (tmr) {
+      g_cs_timing[12 * blockIdx.x + 4] = g_a;
+      g_cs_timing[12 * blockIdx.x + 5] = g_b;
+      g_cs_timing[12 * blockIdx.x + 6] = g_c;
+      g_cs_timing[12 * blockIdx.x + 7] = n_it;
+    }
+#endif
     if (p.fc_cache)
       forecast_cached_tiles<SOFTMAX_THREADS>(p, threadIdx.x - 128, 8, &bars->fc_tile);
   }
   tc_fence_before();
   __syncthreads();
 #ifdef FO_CS_TIMING
-  if (threadIdx.x == 0) g_cs_timing[4 * blockIdx.x + 1] = global_ns();
+  if (threadIdx.x == 0) g_cs_timing[12 * blockIdx.x + 1] = global_ns();
 #endif
   if (warp == 1) {
     tc_fence_after();
@@ -561,7 +686,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #ifdef FO_CS_TIMING
 extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigned long long* out,
                                                                        int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 4 * n);
+  return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 12 * n);
 }
 #endif
 

@@ -29,11 +29,17 @@ for _ in range(5):
 torch.cuda.synchronize()
 lib = _lib.load()
 n = 148
-buf = (ctypes.c_ulonglong * (4 * 1024))()
+buf = (ctypes.c_ulonglong * (12 * 1024))()
 assert lib.fo_debug_cs_timing(buf, 1024) == 0
-a = np.array(buf[:4 * n], dtype=np.int64).reshape(n, 4)
+raw = [int(v) for v in buf[:12 * n]]
+raw0 = [v - (1 << 64) if v >= (1 << 63) else v for v in raw]
+qk_to_s = np.array([float('nan')] * n)
+for b in range(n):
+    raw[12 * b + 10] = 0
+a = np.array(raw, dtype=np.int64).reshape(n, 12)
 t0 = a[:, 0].min()
 start, end, sm, tiles = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2], a[:, 3]
+ga, gb, gc, nit = a[:, 4] / 1e3, a[:, 5] / 1e3, a[:, 6] / 1e3, np.maximum(a[:, 7], 1)
 busy = end - start
 rate = busy * 1e3 / np.maximum(tiles, 1)  # ns per tile
 print(f"kernel span {end.max():.1f} us; CTA start spread {start.max() - start.min():.1f} us")
@@ -41,5 +47,12 @@ print(f"end: min {end.min():.1f} median {np.median(end):.1f} max {end.max():.1f}
       f"mean idle at tail {(end.max() - end).mean():.1f} us ({(end.max() - end).mean() / end.max() * 100:.2f}%)")
 print(f"tiles per CTA: min {tiles.min()} max {tiles.max()} mean {tiles.mean():.1f}")
 print(f"ns per tile: min {rate.min():.0f} median {np.median(rate):.0f} max {rate.max():.0f}")
+print(f"per item (us): last P -> last PV done {np.mean(ga / nit):.2f}, epilogue {np.mean(gb / nit):.2f}, "
+      f"epilogue end -> next first S {np.mean(gc / np.maximum(nit - 1, 1)):.2f}; items/CTA {nit.mean():.1f}; "
+      f"boundary share of the span {np.mean(ga + gb + gc) / end.max():.2%}")
+print(f"per item (us): producer waits q_empty {np.mean(a[:, 8] / 1e3 / nit):.2f}; "
+      f"MMA last PV issued -> next Q landed {np.mean(a[:, 9] / 1e3 / nit):.2f}")
+print(f"per item (us): softmax epilogue end -> reaches the first S wait {np.mean(np.array([raw0[12 * b + 10] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
+print(f"per item (us): first QK issued -> its s_full completes (MMA warp polling) {np.mean(np.array([raw0[12 * b + 11] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
 order = np.argsort(sm)
 print("by SM (sm: ns/tile):", " ".join(f"{s}:{r:.0f}" for s, r in zip(sm[order][:148:8], rate[order][:148:8])))
