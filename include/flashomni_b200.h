@@ -20,6 +20,9 @@
  *   s_c               uint8 [heads, ceil(ceil(rows/pool_n)/8)]
  *   s_s               uint8 [heads, ceil(rows/pool_n), ceil(ceil(cols/pool_n)/8)]
  * Blocks are b_q = b_k = 128 tokens; rows = cols = ceil(seq/128).
+ * Alignment: TMA-read operands start on a 16-byte boundary; the outputs
+ * written with 256-bit row stores (attention out, GEMM-Q q_out, GEMM-O
+ * update out and bias) on a 32-byte boundary (FO_ERR_PARAM otherwise).
  */
 #ifndef FLASHOMNI_B200_H
 #define FLASHOMNI_B200_H

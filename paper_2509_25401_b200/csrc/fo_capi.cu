@@ -62,6 +62,14 @@ int make_map_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, 
 }
 
 // box = 64 columns (128 B) x box_rows, SW128: the MMA operand tiles
+// outputs written by row-per-thread 256-bit stores (attention O, GEMM-Q,
+// GEMM-O update out / bias) must start on a 32-byte boundary
+static int check_align32(const void* ptr, const char* name) {
+  if (ptr && (reinterpret_cast<uintptr_t>(ptr) & 31) != 0)
+    return fail(FO_ERR_PARAM, "%s: base address not 32-byte aligned", name);
+  return FO_OK;
+}
+
 int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
              const char* name) {
   return make_map_ex(m, base, rows, cols, 64, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, name);
@@ -210,6 +218,7 @@ static int attention_common(const void* q, const void* k, const void* v, int seq
   if (rc) return rc;
   rc = check_symbol_dims(heads, rows, cols, pool_n);
   if (rc) return rc;
+  if ((rc = check_align32(out, "out"))) return rc;
   if (seq < 1) return fail(FO_ERR_SHAPE, "empty sequence");
   const int t = ceil_div_d(seq, kTile);
   if (rows != t || cols != t)
@@ -346,6 +355,7 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (d_model % 64 != 0 || d_model < 64) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 64");
+  if ((rc = check_align32(q_out, "q_out"))) return rc;
   if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64]");
   if (!dense && !plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
   CUtensorMap xm, wm;
@@ -431,6 +441,7 @@ int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int s
                          cm, wm);
   if (rc) return rc;
   if (order_d > 0 && !cache) return fail(FO_ERR_PARAM, "order_d > 0 needs the diff-stack cache");
+  if ((rc = check_align32(out, "out")) || (rc = check_align32(bias, "bias"))) return rc;
   p.update = 1;
   p.out = static_cast<__nv_bfloat16*>(out);
   p.bias = static_cast<__nv_bfloat16*>(bias);

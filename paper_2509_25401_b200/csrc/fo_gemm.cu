@@ -100,17 +100,18 @@ __device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
   for (int k = 0; k < N; ++k) asm volatile("" : "+r"(r[k]));
 }
 
+// 32 bf16 of one row (64 B, 32-B aligned) as two 256-bit stores
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
+  uint4 pk[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint4 pk;
-    pk.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-    pk.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-    pk.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-    pk.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-    d[q] = pk;
+    pk[q].x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+    pk[q].y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+    pk[q].z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+    pk[q].w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
   }
+  st_global_256(dst, pk[0], pk[1]);
+  st_global_256(dst + 16, pk[2], pk[3]);
 }
 }  // namespace gemm
 
