@@ -65,6 +65,10 @@ FO_API int fo_num_sms(void);
  * offsets of {counts, items, gemm-q tiles, head masks, orders, pairs, gemm-q head-pair jobs}. */
 FO_API size_t fo_plan_workspace_bytes(int heads, int rows);
 FO_API void fo_plan_offsets(int heads, int rows, size_t offsets[7]);
+/* Byte offset of the attention schedule in the plan workspace: int32
+ * [n_waves, num_sms], the item each CTA runs in each wave (-1: none);
+ * n_waves is counts[6]. */
+FO_API size_t fo_plan_schedule_offset(int heads, int rows);
 
 /* K1 symbol pack. Replaces encode_cache_mask / encode_skip_mask / build_symbols
  * (reference pkg/src/omniattn/symbols.py:65-81,145-160) for all heads at once.

@@ -32,6 +32,7 @@ SIGNATURES = {
     "fo_num_sms": [],
     "fo_plan_workspace_bytes": [_I, _I],
     "fo_plan_offsets": [_I, _I, _P],
+    "fo_plan_schedule_offset": [_I, _I],
     "fo_encode_symbols": [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P],
     "fo_decode_symbols": [_P, _P, _I, _I, _I, _I, _P, _P, _P],
     "fo_plan": [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P],
@@ -51,7 +52,8 @@ SIGNATURES = {
     "fo_generate_masks": [_P, _P, _I, _I, _I, _I, _D, _D, _D, _I, _P, _P, _P, _SZ, _P],
 }
 _RESTYPES = {"fo_last_error": ctypes.c_char_p, "fo_plan_workspace_bytes": _SZ,
-             "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ}
+             "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ,
+             "fo_plan_schedule_offset": _SZ}
 
 # return codes / status bits (flashomni_b200.h)
 _CODE_ERRORS = {1: ShapeError, 2: ParameterError, 3: BoundsError, 4: ConsistencyError,

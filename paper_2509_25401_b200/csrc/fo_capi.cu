@@ -146,6 +146,12 @@ int fo_num_sms(void) { return num_sms(); }
 
 size_t fo_plan_workspace_bytes(int heads, int rows) { return plan_layout(heads, rows, nullptr, nullptr); }
 
+size_t fo_plan_schedule_offset(int heads, int rows) {
+  PlanView pv;
+  plan_layout(heads, rows, nullptr, &pv);
+  return reinterpret_cast<size_t>(pv.att_sched);
+}
+
 void fo_plan_offsets(int heads, int rows, size_t offsets[7]) {
   PlanView pv;
   plan_layout(heads, rows, nullptr, &pv);

@@ -74,6 +74,15 @@ class Plan:
     def pairs_pred(self):
         return self._view(5, torch.int64, self.heads).cpu().numpy()
 
+    def schedule(self):
+        """Attention schedule: int32 [n_waves, num_sms], the item index (into
+        items()) each CTA runs in each wave, -1 for none."""
+        lib = _lib.load()
+        off = int(lib.fo_plan_schedule_offset(self.heads, self.rows))
+        n_waves, ctas = int(self.counts()[6]), int(lib.fo_num_sms())
+        n = n_waves * ctas
+        return self.ws[off:off + 4 * n].view(torch.int32).cpu().numpy().reshape(n_waves, ctas)
+
     def gq_pairs(self):
         """GEMM-Q jobs: (block, head1, head2 or -1), one N=256 (or 128) tile each."""
         n = int(self._view(0, torch.int32, 8)[4].item())
