@@ -259,9 +259,9 @@ class _Layer:
                                  torch.zeros(H, cr, ceil_div(cc, 8), dtype=torch.uint8,
                                              device=device), t, t, pool)
         nbytes = _lib.load().fo_plan_workspace_bytes(H, t)
-        # plan_g: no cache check (GEMM-Q, GEMM-O dispatch); plan_c: with the
-        # cache's valid orders (attention cold-cache check, GEMM-O update orders)
-        self.plan_g = Plan(torch.zeros(nbytes, dtype=torch.uint8, device=device), H, t, False)
+        # one plan per window, built with the cache's valid orders (attention
+        # cold-cache check, GEMM-O update orders); GEMM-Q and GEMM-O dispatch
+        # read only its tile lists and head masks, which valid does not change
         self.plan_c = Plan(torch.zeros(nbytes, dtype=torch.uint8, device=device), H, t, False)
         self.bias = CachedBias(stacks=torch.zeros(cfg.order_d + 1, S, dm, **bf),
                                orders=torch.zeros(t, dtype=torch.int32, device=device),
@@ -288,7 +288,6 @@ class _Layer:
                                check=False)
         Plan.build(self.sym, valid=self.cache.valid, order_d=cfg.order_d, status=status,
                    check=False, ws=self.plan_c.ws)
-        Plan.build(self.sym, status=status, check=False, ws=self.plan_g.ws)
         project_out_update(self.o, p.w_out, self.sym, self.cache, cfg.order_d, out=self.out,
                            bias=self.bias, plan=self.plan_c, status=status, check=False)
         self.ready = True
@@ -308,14 +307,14 @@ class _Layer:
 
     def dispatch(self, x, elapsed_k, status):
         cfg, p = self.cfg, self.params
-        project_q(x, p.w_q, p.q_norm, self.sym, "dispatch", out=self.q, plan=self.plan_g,
+        project_q(x, p.w_q, p.q_norm, self.sym, "dispatch", out=self.q, plan=self.plan_c,
                   status=status, check=False)
         project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
         sparse_attention(self.q, self.k, self.v, self.sym, self.cache, None, elapsed_k,
                          cfg.interval_n, cfg.order_d, mode="bias", out=self.o, plan=self.plan_c,
                          pairs=self.pairs, status=status, check=False)
         project_out_dispatch(self.o, p.w_out, self.sym, self.bias, elapsed_k, cfg.interval_n,
-                             cfg.order_d, out=self.out, plan=self.plan_g, status=status,
+                             cfg.order_d, out=self.out, plan=self.plan_c, status=status,
                              check=False)
         return self.out
 

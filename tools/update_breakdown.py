@@ -31,10 +31,9 @@ for rep in range(2):
     dense_attention_update(L.q, L.k, L.v, L.cache, out=L.o, check=False)
     ev[5].record()
     Plan.build(L.sym, valid=L.cache.valid, order_d=1, check=False, ws=L.plan_c.ws)
-    Plan.build(L.sym, check=False, ws=L.plan_g.ws)
     ev[6].record()
     project_out_update(L.o, p.w_out, L.sym, L.cache, 1, out=L.out, bias=L.bias, plan=L.plan_c, check=False)
     ev[7].record()
     torch.cuda.synchronize()
-names = ["gemm_q", "kv", "policy", "encode", "dense_attn+push", "plans", "gemm_o_update"]
+names = ["gemm_q", "kv", "policy", "encode", "dense_attn+push", "plan", "gemm_o_update"]
 print({n: round(ev[i].elapsed_time(ev[i+1]), 3) for i, n in enumerate(names)})
