@@ -196,17 +196,35 @@ scores_kernel(const float* __restrict__ pq, const float* __restrict__ pk, int ro
 // Ranks by (value, index) in parallel; one lane scans the fp64 cumsum in rank
 // order. Returns cut: elements with rank < cut are taken.
 template <bool CTA>
-__device__ int budget_prefix(const double* v, int n, double budget, bool relative, int* rank,
-                             double* sorted, int tid, int nt) {
-  for (int i = tid; i < n; i += nt) {
-    const double vi = v[i];
-    int rk = 0;
-    for (int j = 0; j < n; ++j) {
-      const double vj = v[j];
-      rk += (vj < vi) || (vj == vi && j < i);
+__device__ int budget_prefix(const double* v, float* vf, int n, double budget, bool relative,
+                             int* rank, double* sorted, int tid, int nt) {
+  // ranks compare fp32 copies (v holds fp32 values, so the order is the same)
+  // with up to eight elements per thread in registers against one broadcast read
+  for (int i = tid; i < n; i += nt) vf[i] = (float)v[i];
+  if (CTA) __syncthreads(); else __syncwarp();
+  constexpr int kU = CTA ? 1 : 8;  // elements per thread (a CTA has 256 threads for <= 1024)
+  for (int i0 = tid; i0 < n; i0 += kU * nt) {
+    float vi[kU];
+    int rk[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * nt;
+      vi[u] = i < n ? vf[i] : INFINITY;
+      rk[u] = 0;
     }
-    rank[i] = rk;
-    sorted[rk] = vi;
+    for (int j = 0; j < n; ++j) {
+      const float vj = vf[j];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) rk[u] += (vj < vi[u]) | ((vj == vi[u]) & (j < i0 + u * nt));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * nt;
+      if (i < n) {
+        rank[i] = rk[u];
+        sorted[rk[u]] = v[i];
+      }
+    }
   }
   if (CTA) __syncthreads(); else __syncwarp();
   int cut = 0;
@@ -254,6 +272,7 @@ cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, doub
       (reinterpret_cast<uintptr_t>(cc + rows_c) + 7) & ~uintptr_t(7));
   float* tmp = reinterpret_cast<float*>(e + rows_c);           // [V]
   float* acc = tmp + rows_c;                                   // [V]
+  float* vf = acc + rows_c;                                    // [V] rank keys
   // vision_to_text_contribution: p[:n_t, n_t:].sum(axis=0), fp32 row by row
   for (int c = tid; c < V; c += nt) {
     float a = 0.f;
@@ -293,10 +312,10 @@ cache_select_kernel(const float* __restrict__ p_tilde, int rows_c, int n_t, doub
   for (int c = tid; c < V; c += nt) guid[c] = n_t > 0 ? (double)acc[c] : 0.0;
   __syncthreads();
   // select_cached_blocks: both ascending prefixes within tau_q of their totals
-  int cut = budget_prefix<true>(contrib, V, tau_q, true, rank, sorted, tid, nt);
+  int cut = budget_prefix<true>(contrib, vf, V, tau_q, true, rank, sorted, tid, nt);
   for (int i = tid; i < V; i += nt) cut_c[i] = rank[i] < cut;
   __syncthreads();
-  cut = budget_prefix<true>(guid, V, tau_q, true, rank, sorted, tid, nt);
+  cut = budget_prefix<true>(guid, vf, V, tau_q, true, rank, sorted, tid, nt);
   for (int r = tid; r < rows_c; r += nt)
     cc[r] = (r < n_t) ? 1 : !(cut_c[r - n_t] && rank[r - n_t] < cut);
   __syncthreads();
@@ -326,10 +345,11 @@ __global__ void skip_select_kernel(const float* __restrict__ p_tilde,
   if (gw >= H * rows_c) return;
   const int cols = rows_c, t_kv = t_q;
   const int h = gw / rows_c, r = gw % rows_c;
-  double* v = sk_smem + (size_t)wib * cols * 3;  // candidate scores
+  double* v = sk_smem + (size_t)wib * cols * 4;  // candidate scores
   double* sorted = v + cols;
   int* rank = reinterpret_cast<int*>(sorted + cols);
-  uint8_t* keep = reinterpret_cast<uint8_t*>(rank + cols);
+  float* vf = reinterpret_cast<float*>(rank + cols);
+  uint8_t* keep = reinterpret_cast<uint8_t*>(vf + cols);
   const bool active = comp_cache[(size_t)h * rows_c + r] != 0;
   const float* P = p_tilde + ((size_t)h * rows_c + r) * cols;
   // guarded: text columns and the diagonal are protected (square map: r < cols)
@@ -347,7 +367,7 @@ __global__ void skip_select_kernel(const float* __restrict__ p_tilde,
   if (active && nc > 0) {
     for (int k = lane; k < nc; k += 32) v[k] = (double)P[cand_col(k)];
     __syncwarp();
-    const int cut = budget_prefix<false>(v, nc, tau_kv, false, rank, sorted, lane, 32);
+    const int cut = budget_prefix<false>(v, vf, nc, tau_kv, false, rank, sorted, lane, 32);
     int spare = -1;
     if (!any_prot && cut == nc) {  // all skipped: spare argmax (first occurrence)
       if (lane == 0) {
@@ -403,9 +423,9 @@ cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k
   scores_kernel<<<dim3((rows_c + rows_cta - 1) / rows_cta, H), kScWarps * 32, sm_sc, stream>>>(
       pq, pk, rows_c, pt);
   const int grid_rows = (H * rows_c + kPolWarps - 1) / kPolWarps;
-  const size_t sm_rows = (size_t)kPolWarps * rows_c * 3 * sizeof(double);
+  const size_t sm_rows = (size_t)kPolWarps * rows_c * 4 * sizeof(double);
   const size_t sm_cache =
-      (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2) + 8 + (size_t)rows_c * (8 + 4 + 4);
+      (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2) + 8 + (size_t)rows_c * (8 + 4 + 4 + 4);
   cudaFuncSetAttribute(cache_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm_cache);
   cache_select_kernel<<<H, 256, sm_cache, stream>>>(pt, rows_c, n_t, tau_q, s_q, cc);
