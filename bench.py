@@ -75,12 +75,28 @@ def random_masks(rng, heads, t, cached_ratio, skip_ratio):
 
 
 def peaks():
+    """(bf16 burst TFLOP/s, bf16 sustained TFLOP/s, HBM GB/s, source) from the
+    driver's MEASURED_PEAKS.json (keys as B200_PROFILING.md names them, at the
+    top level or one level down), else the recipe's fallback."""
+    fallback = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
     p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get(
-            "hbm_gbs", 6650.0), "measured"
-    return 1590.0, 1400.0, 6650.0, "fallback"
+    if not p.exists():
+        return (*fallback.values(), "fallback")
+    d = json.loads(p.read_text())
+    flat = dict(d)
+    for v in d.values():
+        if isinstance(v, dict):
+            for k, x in v.items():
+                flat.setdefault(k, x)
+    got, src = [], "measured"
+    for k, fb in fallback.items():
+        v = flat.get(k)
+        if isinstance(v, (int, float)) and v > 0:
+            got.append(float(v))
+        else:
+            got.append(fb)
+            src = "measured (fallback for missing keys)"
+    return (*got, src)
 
 
 # ---------------------------------------------------------------------------
