@@ -118,10 +118,13 @@ def test_gpu_policy_matches_reference_fixture(case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("pool_n,n,n_text,heads", [(1, 2304, 256, 4), (2, 2944, 384, 3),
-                                                   (3, 2000, 0, 2), (1, 33024, 512, 2)])
+                                                   (3, 2000, 0, 2), (1, 33024, 512, 2),
+                                                   (1, 131072, 512, 1)])
 def test_gpu_policy_batched_heads_match_oracle(pool_n, n, n_text, heads):
-    """All heads in one call equal the oracle run head by head; the last case
-    is the bench workload's sequence (258 x 258 compressed map)."""
+    """All heads in one call equal the oracle run head by head; (1, 33024) is
+    the bench workload's sequence (258 x 258 compressed map) and (1, 131072)
+    the largest map the kernels take (1024 x 1024: 16 score chunks, 176 KB of
+    shared memory per CTA)."""
     import torch
 
     import paper_2509_25401_b200 as fo
