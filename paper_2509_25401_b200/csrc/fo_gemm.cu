@@ -20,6 +20,12 @@
 
 #include "fo_internal.cuh"
 
+// GEMM-O dispatch: the bias stream and the output are touched once, so they go
+// through L2 as evict-first and leave W and o (re-read by every row block) in L2
+#ifndef FO_GO_EVICT_FIRST
+#define FO_GO_EVICT_FIRST 1
+#endif
+
 namespace fo {
 namespace gemm {
 constexpr int BM = 128, BN = 128, BK = 64;
@@ -788,8 +794,13 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           uint8_t* slot = ring + rb.s * BIAS_SLOT_BYTES;
           mbar_arrive_expect_tx(&bars->bfull[rb.s], ns * BIAS_ORDER_BYTES);
           for (int dd = 0; dd < ns; ++dd)
+#if FO_GO_EVICT_FIRST
+            tma_load_2d_hint(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s],
+                             nb * TBN + c * 32, dd * p.S + i * BM, l2_evict_first_policy());
+#else
             tma_load_2d(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s], nb * TBN + c * 32,
                         dd * p.S + i * BM);
+#endif
         }
         __syncwarp();
         rb.next();
@@ -932,7 +943,12 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           named_bar_sync(1, 128);
           if (warp == 4) {
             if (elect_one()) {
+#if FO_GO_EVICT_FIRST
+              tma_store_2d_hint(&om, ostage + ob * OUT_STAGE_BYTES, nb * TBN + c * 32, i * BM,
+                                l2_evict_first_policy());
+#else
               tma_store_2d(&om, ostage + ob * OUT_STAGE_BYTES, nb * TBN + c * 32, i * BM);
+#endif
               bulk_commit();
               bulk_wait_read<1>();  // the other staging buffer's store has read it
             }
