@@ -151,9 +151,11 @@ FO_API int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int 
               const float* norm_w, const float* rope_cos, const float* rope_sin, float eps,
               const void* plan_ws, int dense, void* q_out, void* stream);
 
-/* K5 GEMM-O update: out = sum_h o_h W_h, B_c[d] = sum_{h cached next} stack_d^h W_h
- * (gemm.py:110-175). plan_ws is the plan of the NEXT symbols built with `valid`;
- * orders are taken from it. */
+/* K5 GEMM-O update: B_c[d] = sum_{h cached next} stack_d^h W_h and
+ * out = B_c[0] + sum_{h active next} o_h W_h (gemm.py:110-175): cached heads'
+ * order-0 term comes from the cache's stack 0, not from o. cache is
+ * [cache_order+1, seq, heads*128] (required: STATE when NULL). plan_ws is the
+ * plan of the NEXT symbols built with `valid`; orders are taken from it. */
 FO_API int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int seq, int heads,
                      int head_dim, int d_model, int order_d, const void* plan_ws, void* out,
                      void* bias, uint32_t* status, void* stream);

@@ -29,7 +29,13 @@ def as_device(t, dtype, name):
 
 
 def check_bsd(t, name, seq=None, heads=None):
-    """[S, H, 128] token-major activations (a [S, H*128] view is accepted)."""
+    """[S, H, 128] token-major bf16 activations on the GPU (a [S, H*128] view is
+    accepted). The kernels' TMA maps assume a dense row stride of H*128, so a
+    strided view (e.g. a head slice q[:, :2]) is copied to a dense tensor."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.bfloat16:
+        raise ParameterError(f"{name}: expected a CUDA bf16 tensor")
+    if not t.is_contiguous():
+        t = t.contiguous()
     if t.dim() == 2:
         if t.shape[1] % TILE:
             raise ShapeError(f"{name}: width {t.shape[1]} not a multiple of {TILE}")
@@ -43,6 +49,30 @@ def check_bsd(t, name, seq=None, heads=None):
     if heads is not None and t.shape[1] != heads:
         raise ShapeError(f"{name}: heads {t.shape[1]} != {heads}")
     return t
+
+
+def check_out(t, name, shape, dtype=torch.bfloat16, device=None):
+    """Validate a caller-supplied output buffer before a kernel writes into it:
+    exact shape, dtype, device and a dense layout (an undersized or strided
+    buffer would otherwise be written out of bounds / at the wrong rows)."""
+    if not isinstance(t, torch.Tensor):
+        raise ParameterError(f"{name}: expected a torch tensor")
+    if tuple(t.shape) != tuple(shape) and not (t.numel() == _numel(shape) and t.dim() != len(shape)):
+        raise ShapeError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ParameterError(f"{name}: dtype {t.dtype} != {dtype}")
+    if not t.is_cuda or (device is not None and t.device != torch.device(device)):
+        raise ParameterError(f"{name}: must live on {device or 'the CUDA device'}, got {t.device}")
+    if not t.is_contiguous():
+        raise ParameterError(f"{name}: must be contiguous (kernels write a dense row stride)")
+    return t
+
+
+def _numel(shape):
+    n = 1
+    for s in shape:
+        n *= int(s)
+    return n
 
 
 class Status:

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._runtime import TILE, Status, check_bsd, check_finite, require_cuda, stream_ptr
+from ._runtime import TILE, Status, check_bsd, check_finite, check_out, require_cuda, stream_ptr
 from .errors import ParameterError, ShapeError, StateError
 from .symbols import DeviceSymbols, SymbolBuffer, ceil_div
 
@@ -208,8 +208,6 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
         raise ShapeError(f"symbols dimensioned {symbols.rows}x{symbols.cols}, expected {t_q}x{t_q}")
     if symbols.heads != heads:
         raise ShapeError(f"symbols for {symbols.heads} heads, q has {heads}")
-    if mode == "materialize":
-        check_elapsed(elapsed_k, interval_n)
     st = status or Status.default()
     if cache is not None:
         if (cache.heads, cache.n_blocks) != (heads, t_q):
@@ -221,6 +219,13 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     if plan is None:
         plan = symbols.plan(valid=valid, valid_version=vver, order_d=order_d, status=st,
                             stream=stream, check=check)
+    if mode == "materialize" and (interval_n < 1 or not 1 <= elapsed_k <= interval_n - 1):
+        # the reference validates elapsed_k inside forecast(), i.e. only for a
+        # cached block and after its cold-cache StateError (attention.py:104-107,
+        # 208-216): all-active symbols with any elapsed_k are legal
+        if int(plan.counts()[1]) < heads * t_q:
+            st.check("sparse_attention")
+            check_elapsed(elapsed_k, interval_n)
     if check:
         # as_matrix (tensor.py:19-30): q only on the rows it reads (attention.py:176-196)
         check_finite(q, "q: active-block rows", st, plan=plan, stream=stream)
@@ -229,6 +234,8 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     if out is None:
         out = torch.full((seq, heads, TILE), float(fill) if fill is not None else 0.0,
                          dtype=torch.bfloat16, device=q.device)
+    else:
+        check_out(out, "out", (seq, heads, TILE), device=q.device)
     if pairs is None and counters is not None:
         pairs = torch.zeros(heads, dtype=torch.int64, device=q.device)
     if mode == "materialize" and cache is not None and cache.stacks is not None:
@@ -276,6 +283,8 @@ def dense_attention_update(q, k, v, cache, *, out=None, counters=None, stream=No
             check_finite(t, name, st, stream=stream)
     if out is None:
         out = torch.empty(seq, heads, TILE, dtype=torch.bfloat16, device=q.device)
+    else:
+        check_out(out, "out", (seq, heads, TILE), device=q.device)
     pairs = torch.zeros(heads, dtype=torch.int64, device=q.device) if counters is not None else None
     _lib.call("fo_sparse_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), seq, heads, TILE,
               plan.sym.s_s.data_ptr(), t_q, t_q, 1, plan.ptr(), 1.0 / math.sqrt(TILE),

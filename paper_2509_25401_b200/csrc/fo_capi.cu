@@ -311,6 +311,8 @@ int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim,
   if (rc) return rc;
   if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
   if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
+  if (!cache || !valid || !coef || !plan_ws || !out)
+    return fail(FO_ERR_PARAM, "forecast_materialize: NULL operand");
   float c[4] = {0, 0, 0, 0};
   for (int d = 0; d <= order_d; ++d) c[d] = coef[d];
   PlanView pv = plan_view(plan_ws, heads, rows);
@@ -446,7 +448,7 @@ int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int s
   int rc = gemm_o_common(o, cache, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p, am,
                          cm, wm);
   if (rc) return rc;
-  if (order_d > 0 && !cache) return fail(FO_ERR_PARAM, "order_d > 0 needs the diff-stack cache");
+  if (!cache) return fail(FO_ERR_STATE, "update projection needs the refreshed feature cache");
   if ((rc = check_align32(out, "out")) || (rc = check_align32(bias, "bias"))) return rc;
   p.update = 1;
   p.out = static_cast<__nv_bfloat16*>(out);
@@ -464,7 +466,9 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
   int rc = gemm_o_common(o, nullptr, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p,
                          am, cm, wm);
   if (rc) return rc;
-  if (!orders) return fail(FO_ERR_STATE, "dispatch projection requires the update-step bias");
+  if (!orders || !bias) return fail(FO_ERR_STATE, "dispatch projection requires the update-step bias");
+  if (!coef) return fail(FO_ERR_PARAM, "gemm_o_dispatch: coef is NULL");
+  if (!out) return fail(FO_ERR_PARAM, "gemm_o_dispatch: out is NULL");
   p.update = 0;
   p.orders = orders;
   for (int d = 0; d <= order_d; ++d) p.coef[d] = coef[d];

@@ -9,8 +9,9 @@
 // the K loop walks heads, 128 K-columns each.
 //   dispatch: only heads active for block i are multiplied; the epilogue adds
 //             sum_d c_d * B_c[d] (the forecast of the cached-head bias).
-//   update:   job (i, n, d). d=0 accumulates cached heads into accumulator B and
-//             active heads into accumulator A in one K pass; B -> B_c[0],
+//   update:   job (i, n, d). d=0 accumulates cached heads (their cache stack 0)
+//             into accumulator B and active heads (o) into accumulator A in one
+//             K pass; B -> B_c[0],
 //             A + B -> out. d>=1 projects the cached heads' d-th difference
 //             stacks into B_c[d]. Every head is projected exactly once.
 // Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..7 epilogue
@@ -687,8 +688,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           unsigned long long m;
           if (pass == 0) m = UPDATE ? cached : 0ull;
           else m = (d == 0) ? act : 0ull;
-          const CUtensorMap* src = (UPDATE && pass == 0 && d > 0) ? &cm : &am;
-          const int row0 = (UPDATE && pass == 0 && d > 0) ? d * p.S + i * BM : i * BM;
+          // cached heads read the cache's difference stack d, order 0 included
+          // (gemm.py:155-161 projects entry.diff_stack[dd] for every dd)
+          const CUtensorMap* src = (UPDATE && pass == 0) ? &cm : &am;
+          const int row0 = (UPDATE && pass == 0) ? d * p.S + i * BM : i * BM;
           while (m) {
             const int h = __ffsll(m) - 1;
             m &= m - 1;

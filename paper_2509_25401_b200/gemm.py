@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._runtime import TILE, Status, as_device, check_bsd, check_finite, require_cuda, stream_ptr
+from ._runtime import (TILE, Status, as_device, check_bsd, check_finite, check_out, require_cuda,
+                       stream_ptr)
 from .attention import check_elapsed, ctypes_floats, forecast_coefficients
 from .errors import ParameterError, ShapeError, StateError
 from .symbols import DeviceSymbols, ceil_div
@@ -132,6 +133,8 @@ def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, 
     if out is None:
         out = torch.full((n, heads, TILE), 0.0 if fill is None else float(fill),
                          dtype=torch.bfloat16, device=x.device)
+    else:
+        check_out(out, "out", (n, heads, TILE), device=x.device)
     if phase == "dispatch":
         if symbols is None or symbols.heads != heads or symbols.rows != t_q:
             raise ShapeError(f"symbols must cover {heads} heads x {t_q} blocks")
@@ -206,8 +209,14 @@ def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE
                                  status=st, stream=stream, check=check)
     if out is None:
         out = torch.empty(n, dm, dtype=torch.bfloat16, device=o.device)
-    stacks = bias.stacks if bias is not None else torch.empty(order_d + 1, n, dm,
-                                                              dtype=torch.bfloat16, device=o.device)
+    else:
+        check_out(out, "out", (n, dm), device=o.device)
+    if bias is not None:
+        check_out(bias.stacks, "bias.stacks", (order_d + 1, n, dm), device=o.device)
+        check_out(bias.orders, "bias.orders", (t_q,), dtype=torch.int32, device=o.device)
+        stacks = bias.stacks
+    else:
+        stacks = torch.empty(order_d + 1, n, dm, dtype=torch.bfloat16, device=o.device)
     # the cache stacks are [cache.order+1, seq, H*128]; the kernel addresses slot d < order_d+1
     _lib.call("fo_gemm_o_update", o.data_ptr(), cache.stacks.data_ptr(), w.t.data_ptr(), n, heads,
               TILE, dm, order_d, plan.ptr(), out.data_ptr(), stacks.data_ptr(), st.ptr(),
@@ -259,8 +268,15 @@ def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, o
     if plan is None:
         plan = symbols.plan(status=st, stream=stream, check=check)
     coef = ctypes_floats(forecast_coefficients(elapsed_k, interval_n, order_d + 1))
+    if bias.stacks.dim() != 3 or bias.stacks.shape[0] < min(order_d, bias.order_d) + 1:
+        raise ShapeError(f"bias.stacks {tuple(bias.stacks.shape)} holds fewer than "
+                         f"{min(order_d, bias.order_d) + 1} orders")
+    check_out(bias.stacks, "bias.stacks", (bias.stacks.shape[0], n, dm), device=o.device)
+    check_out(bias.orders, "bias.orders", (t_q,), dtype=torch.int32, device=o.device)
     if out is None:
         out = torch.empty(n, dm, dtype=torch.bfloat16, device=o.device)
+    else:
+        check_out(out, "out", (n, dm), device=o.device)
     _lib.call("fo_gemm_o_dispatch", o.data_ptr(), w.t.data_ptr(), bias.stacks.data_ptr(),
               bias.orders.data_ptr(), n, heads, TILE, dm, min(order_d, bias.order_d),
               ctypes.addressof(coef), plan.ptr(), out.data_ptr(), stream_ptr(stream))

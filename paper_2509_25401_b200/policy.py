@@ -8,6 +8,11 @@ pipeline.py:254-266. Here all heads run in one C-ABI call
 (`fo_generate_masks`, csrc/fo_policy.cu) whose decisions match the
 reference's float32/float64 numpy bit for bit, and the result feeds
 `encode_symbols` without leaving the device.
+
+Inputs are the engine's bf16 activations: q and k given in another dtype
+(e.g. the reference's float32) are rounded to bf16 before pooling, so the
+decisions are bit-for-bit those the reference makes on the bf16-rounded
+tensors (the fixtures in tests/golden/policy.npz are bf16-representable).
 """
 
 from dataclasses import dataclass

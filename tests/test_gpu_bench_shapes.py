@@ -1,0 +1,308 @@
+"""Parity at the bench's own shapes (BASELINE configs C1, C2, C3/C4).
+
+C4 / C3: S = 33,024 tokens (258 blocks), d_model 3072, 24 heads x 128 — the
+exact GEMM-Q and GEMM-O shapes bench.py times. Full-size outputs are compared
+against the CPU oracle (oracle/, a restatement of gemm.py / attention.py) on
+sampled row blocks: every (block, head) computation is block-local, so a
+subset of blocks, fed to the oracle as a short sequence, is an exact
+restatement of those rows. Tolerance: the stated bf16 bound (conftest.py).
+
+GEMM-Q is checked with symbols that put the plan on the CTA-pair path (>= 70%
+of the active tiles in blocks whose head pair (2p, 2p+1) is active together)
+and with symbols that keep it off; the plan's counters prove which ran.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import assert_bf16_close
+
+pytestmark = pytest.mark.gpu
+
+T = 128
+S_C4, DM, H = 33024, 3072, 24
+T_C4 = S_C4 // T
+
+
+def fo():
+    import paper_2509_25401_b200 as m
+
+    return m
+
+
+def bf16_np(t):
+    return t.float().cpu().numpy()
+
+
+def sample_blocks(rng, t, n=6):
+    """First, last (ragged-free at C4) and a few random blocks."""
+    pick = {0, t - 1}
+    while len(pick) < n:
+        pick.add(int(rng.integers(t)))
+    return np.array(sorted(pick))
+
+
+def rows_of(blocks, seq):
+    return np.concatenate([np.arange(b * T, min(b * T + T, seq)) for b in blocks])
+
+
+def cache_masks(rng, heads, t, cached_ratio):
+    active = rng.random((heads, t)) >= cached_ratio
+    for h in range(heads):
+        if not active[h].any():
+            active[h, rng.integers(t)] = True
+    return active
+
+
+# ---------------------------------------------------------------------------
+# GEMM-Q at C4, CTA-pair path on / off
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("cached_ratio,pairs_expected", [(0.1, True), (0.5, False), (0.9, False)])
+def test_gemm_q_c4_dispatch(cached_ratio, pairs_expected):
+    m = fo()
+    torch.manual_seed(21)
+    rng = np.random.default_rng(int(cached_ratio * 100))
+    x = torch.randn(S_C4, DM, device="cuda").bfloat16()
+    w_q = (torch.randn(H, DM, T, device="cuda") * DM ** -0.5).bfloat16().float()
+    norm = 1 + 0.05 * torch.randn(H, T, device="cuda")
+    active = cache_masks(rng, H, T_C4, cached_ratio)
+    sym = m.encode_symbols(active, np.ones((H, T_C4, T_C4), bool) & active[:, :, None], 1)
+    plan = sym.plan()
+    n_pair_jobs = int(plan.counts()[7])
+    assert (n_pair_jobs > 0) == pairs_expected, n_pair_jobs
+    gc = m.GemmCounters()
+    q = m.project_q(x, w_q, norm, sym, "dispatch", fill=float("nan"), counters=gc)
+    torch.cuda.synchronize()
+    assert gc.q_macs_actual == int(active.sum()) * T * DM * T
+    blocks = sample_blocks(rng, T_C4)
+    rows = rows_of(blocks, S_C4)
+    want = oracle.project_q(bf16_np(x)[rows], w_q.cpu().numpy(), norm.cpu().numpy(),
+                            active[:, blocks], T, positions=rows, fill=np.nan)
+    got = bf16_np(q[torch.from_numpy(rows).cuda()])
+    for h in range(H):
+        sel = np.repeat(active[h, blocks], T)
+        if sel.any():
+            assert_bf16_close(got[sel, h], want[h][sel], f"head {h}")
+        assert np.isnan(got[~sel, h]).all(), "skipped tiles keep the fill"
+
+
+def test_gemm_q_c4_update_phase():
+    m = fo()
+    torch.manual_seed(22)
+    rng = np.random.default_rng(22)
+    x = torch.randn(S_C4, DM, device="cuda").bfloat16()
+    w_q = (torch.randn(H, DM, T, device="cuda") * DM ** -0.5).bfloat16().float()
+    norm = 1 + 0.05 * torch.randn(H, T, device="cuda")
+    q = m.project_q(x, w_q, norm, None, "update")
+    blocks = sample_blocks(rng, T_C4)
+    rows = rows_of(blocks, S_C4)
+    want = oracle.project_q(bf16_np(x)[rows], w_q.cpu().numpy(), norm.cpu().numpy(), None, T,
+                            positions=rows)
+    got = bf16_np(q[torch.from_numpy(rows).cuda()])
+    for h in range(H):
+        assert_bf16_close(got[:, h], want[h], f"head {h}")
+
+
+# ---------------------------------------------------------------------------
+# GEMM-O update + dispatch at C3/C4, orders 0..3
+# ---------------------------------------------------------------------------
+def _filled_cache(m, rng, order, seq=S_C4, heads=H):
+    """order+1 pushes: every entry's valid order is order+1, except a random
+    subset pushed one time fewer (mixed valid orders per block)."""
+    t = seq // T
+    fc = m.FeatureCache(heads, t, order, seq=seq)
+    hist = []
+    for r in range(order + 1):
+        o = torch.randn(seq, heads, T, device="cuda").bfloat16()
+        sel = None if r == 0 or r < order else (rng.random((heads, t)) < 0.7).astype(np.uint8)
+        fc.push(o, select=sel)
+        hist.append(o)
+    return fc, hist
+
+
+def _oracle_stacks(fc, blocks, heads):
+    """Per-head, per-sampled-block diff stacks and valid orders from the
+    device cache (the oracle consumes the cache state, not its history)."""
+    st = fc.stacks.float().view(fc.order + 1, fc.seq, heads, T)
+    valid = fc.valid.cpu().numpy()
+    stacks = [[None] * len(blocks) for _ in range(heads)]
+    vsub = np.zeros((heads, len(blocks)), int)
+    for bi, b in enumerate(blocks):
+        tile = st[:, b * T:(b + 1) * T].cpu().numpy()  # [order+1, 128, heads, 128]
+        for h in range(heads):
+            stacks[h][bi] = tile[:, :, h]
+            vsub[h, bi] = valid[h, b]
+    return stacks, vsub
+
+
+@pytest.mark.parametrize("order,cached_ratio", [(0, 0.25), (1, 0.25), (1, 0.9), (2, 0.5),
+                                                (3, 0.75)])
+def test_gemm_o_c4_update_and_dispatch(order, cached_ratio):
+    m = fo()
+    torch.manual_seed(30 + order)
+    rng = np.random.default_rng(30 + order)
+    w_out = (torch.randn(H, T, DM, device="cuda") * T ** -0.5).bfloat16().float()
+    fc, hist = _filled_cache(m, rng, order)
+    # o != the cache's stack 0: the update must take cached heads' order-0
+    # term from the cache (gemm.py:155-161), active heads from o
+    o = torch.randn(S_C4, H, T, device="cuda").bfloat16()
+    active = cache_masks(rng, H, T_C4, cached_ratio)
+    sym = m.encode_symbols(active, np.ones((H, T_C4, T_C4), bool) & active[:, :, None], 1)
+    gc = m.GemmCounters()
+    out_u, bias = m.project_out_update(o, w_out, sym, fc, order, counters=gc)
+    torch.cuda.synchronize()
+    blocks = sample_blocks(rng, T_C4)
+    rows = rows_of(blocks, S_C4)
+    stacks, vsub = _oracle_stacks(fc, blocks, H)
+    o_sub = bf16_np(o[torch.from_numpy(rows).cuda()]).transpose(1, 0, 2)  # [H, n, 128]
+    wn = w_out.cpu().numpy()
+    want_out, want_bias, want_orders = oracle.project_out_update(
+        o_sub, wn, active[:, blocks].T, stacks, vsub, order, T)
+    got_out = bf16_np(out_u[torch.from_numpy(rows).cuda()])
+    assert_bf16_close(got_out, want_out, f"update out, order {order}")
+    orders = bias.orders.cpu().numpy()
+    assert np.array_equal(orders[blocks], want_orders), "bias orders"
+    bs = bias.stacks.float()
+    for bi, b in enumerate(blocks):
+        for d in range(int(want_orders[bi])):
+            assert_bf16_close(bs[d, b * T:(b + 1) * T].cpu().numpy(), want_bias[bi][d],
+                              f"B_c[{d}] block {b}")
+    # every active head once, every cached head once per populated order
+    full_orders = orders
+    n_cached = (~active).sum(0)
+    assert gc.o_bias_macs == int((n_cached * np.maximum(full_orders - 1, 0)).sum()) * T * T * DM
+
+    # dispatch: active heads of a fresh o plus the forecast of the bias
+    o2 = torch.randn(S_C4, H, T, device="cuda").bfloat16()
+    for elapsed, interval in ((1, 6), (5, 6)):
+        got = m.project_out_dispatch(o2, w_out, sym, bias, elapsed, interval, order)
+        bias_sub = [bs[:int(orders[b]), b * T:(b + 1) * T].cpu().numpy() for b in blocks]
+        o2_sub = bf16_np(o2[torch.from_numpy(rows).cuda()]).transpose(1, 0, 2)
+        want = oracle.project_out_dispatch(o2_sub, wn, active[:, blocks].T, bias_sub,
+                                           orders[blocks], elapsed, interval, order, T)
+        assert_bf16_close(bf16_np(got[torch.from_numpy(rows).cuda()]), want,
+                          f"dispatch out, order {order}, k={elapsed}")
+
+
+def test_gemm_o_update_takes_cached_order0_from_cache():
+    """Small shape, exact structure: with o != cache stack 0, a block whose
+    heads are all cached must equal sum_h stack0_h W_h, and an all-active block
+    sum_h o_h W_h."""
+    m = fo()
+    torch.manual_seed(40)
+    seq, heads, dm = 512, 4, 256
+    t = seq // T
+    w_out = (torch.randn(heads, T, dm, device="cuda") * T ** -0.5).bfloat16().float()
+    fc = m.FeatureCache(heads, t, 0, seq=seq)
+    c0 = torch.randn(seq, heads, T, device="cuda").bfloat16()
+    fc.push(c0)
+    o = torch.randn(seq, heads, T, device="cuda").bfloat16()
+    active = np.ones((heads, t), bool)
+    active[:, 1] = False  # block 1: every head cached
+    active[0, 2] = False  # block 2: one head cached
+    sym = m.encode_symbols(active, np.ones((heads, t, t), bool) & active[:, :, None], 1)
+    out, bias = m.project_out_update(o, w_out, sym, fc, 0)
+    wb = w_out.double()
+    src = torch.where(torch.from_numpy(np.repeat(active.T, T, 0)).cuda()[:, :, None], o, c0)
+    want = sum(src[:, h].double() @ wb[h] for h in range(heads))
+    assert_bf16_close(out.float().cpu().numpy(), want.cpu().numpy(), "update out")
+    b1 = sum(c0[T:2 * T, h].double() @ wb[h] for h in range(heads))
+    assert_bf16_close(bias.stacks[0, T:2 * T].float().cpu().numpy(), b1.cpu().numpy(), "B_c[0]")
+
+
+# ---------------------------------------------------------------------------
+# OP_reuse (forecast) at orders 2 and 3 against oracle.forecast
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("order", [2, 3])
+def test_forecast_orders_2_3_against_oracle(order):
+    m = fo()
+    torch.manual_seed(50 + order)
+    rng = np.random.default_rng(50 + order)
+    n, heads = 1536, 3
+    t = n // T
+    fc = m.FeatureCache(heads, t, order, seq=n)
+    hist = []
+    sels = []
+    for r in range(order + 2):  # one push past the order: the stack saturates
+        o = torch.randn(n, heads, T, device="cuda").bfloat16()
+        sel = np.ones((heads, t), np.uint8) if r == 0 else (rng.random((heads, t)) < 0.8).astype(np.uint8)
+        fc.push(o, select=sel)
+        hist.append(bf16_np(o))
+        sels.append(sel)
+    q, k, v = (torch.randn(n, heads, T, device="cuda").bfloat16() for _ in range(3))
+    cb = np.zeros((heads, t), bool)
+    sb = np.zeros((heads, t, t), bool)
+    for h in range(heads):
+        cb[h], sb[h] = oracle.random_masks(rng, t, t, 1, density=0.5, cache_density=0.4)
+    sym = m.encode_symbols(cb, sb, 1)
+    for elapsed, interval in ((1, 4), (3, 4), (2, 8)):
+        out = m.sparse_attention(q, k, v, sym, fc, None, elapsed, interval, order,
+                                 mode="materialize")
+        of = bf16_np(out)
+        for h in range(heads):
+            for i in range(t):
+                if cb[h, i]:
+                    continue
+                r = slice(i * T, (i + 1) * T)
+                st, vv = None, 0
+                for step, tile in enumerate(hist):
+                    if sels[step][h, i]:
+                        # the device stores each difference in bf16: restate the
+                        # recurrence on the rounded values the cache holds
+                        st, vv = oracle.update_entry(st, vv, tile[r, h], order)
+                want = oracle.forecast(st, vv, elapsed, interval, order)
+                assert int(fc.valid[h, i]) == vv
+                assert_bf16_close(of[r, h], want, f"forecast ({h},{i}) k={elapsed}")
+
+
+# ---------------------------------------------------------------------------
+# attention at C1 (S=4096) and C2 (FLUX, S=4608) shapes
+# ---------------------------------------------------------------------------
+def _attention_check(m, seq, heads, cb, sb, check_heads, seed):
+    torch.manual_seed(seed)
+    t = -(-seq // T)
+    q, k, v = (torch.randn(seq, heads, T, device="cuda").bfloat16() for _ in range(3))
+    sym = m.encode_symbols(cb, sb, 1)
+    fc = m.FeatureCache(heads, t, 0, seq=seq)
+    fc.push(v)
+    ac = m.AttnCounters()
+    out = m.sparse_attention(q, k, v, sym, fc, None, 1, 2, 0, mode="bias", fill=float("nan"),
+                             counters=ac)
+    assert ac.pairs_computed == int(sum(sb[h][cb[h]].sum() for h in range(heads)))
+    assert ac.pairs_total == heads * t * t
+    qf, kf, vf, of = (bf16_np(a) for a in (q, k, v, out))
+    for h in check_heads:
+        want = oracle.masked_attention(qf[:, h], kf[:, h], vf[:, h], cb[h], sb[h], T, T)
+        rows = np.repeat(cb[h], T)[:seq]
+        assert_bf16_close(of[rows, h], want[rows], f"head {h}")
+        assert np.isnan(of[~rows, h]).all()
+
+
+def test_attention_c1():
+    """C1: H=24, S=4096, 25% cached q-blocks, 50% KV skip (verify.py:29-44 rule)."""
+    m = fo()
+    rng = np.random.default_rng(60)
+    t = 32
+    cb = np.zeros((H, t), bool)
+    sb = np.zeros((H, t, t), bool)
+    for h in range(H):
+        cb[h], sb[h] = oracle.random_masks(rng, t, t, 1, density=0.5, cache_density=0.75)
+    _attention_check(m, 4096, H, cb, sb, [0, 7, 23], 60)
+
+
+@pytest.mark.parametrize("sparsity", [0.0, 0.7, 0.9])
+def test_attention_c2_flux(sparsity):
+    """C2: FLUX joint attention, 4,608 tokens (4 text + 32 image blocks), block
+    sparsity sweep; text rows/columns stay dense (the policy's guard)."""
+    m = fo()
+    rng = np.random.default_rng(61 + int(sparsity * 10))
+    t, n_text = 36, 4
+    cb = np.ones((H, t), bool)
+    sb = rng.random((H, t, t)) >= sparsity
+    sb[:, :, :n_text] = True
+    sb[:, :n_text, :] = True
+    for h in range(H):
+        np.fill_diagonal(sb[h], True)
+    _attention_check(m, 4608, H, cb, sb, [0, 11, 23], 61)
