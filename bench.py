@@ -158,91 +158,81 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# reference arm / CPU baseline: the oracle port of the reference CPU path
+# reference arm / CPU baseline: the reference CPU path on the host cores
 # ---------------------------------------------------------------------------
-def cpu_sample(cfg, cache_bits, skip_bits, seed, n_blocks=24):
-    """Time the reference CPU path (oracle port of pyref.py:14-48,
-    gemm.py:44-93,178-229; numpy + OpenBLAS on all host threads) on a bounded
-    sample — `n_blocks` active query blocks of head 0 for attention and
-    GEMM-Q, and the same row blocks (all heads) for GEMM-O dispatch — and scale
-    by exact work counts to one full layer step. Returns (ms, sample text)."""
-    import oracle
+def cpu_layer(args, cfg, cache_bits, skip_bits):
+    """oracle.layer_cpu.CpuLayer: the reference's compiled attention kernel
+    (oracle/_ref, built from /root/reference/.../_core.pyx) over one worker
+    process per host core, plus the numpy GEMM-Q / GEMM-O of gemm.py."""
+    from oracle.layer_cpu import CpuLayer
 
-    rng = np.random.default_rng(seed)
-    S, H, dm = cfg["seq"], cfg["heads"], cfg["d_model"]
-    t = S // T
-    q, k, v = (rng.standard_normal((S, T)).astype(np.float32) for _ in range(3))
-    blocks = np.flatnonzero(cache_bits[0])[:n_blocks]
-    act = np.zeros(t, np.uint8)
-    act[blocks] = 1
-    out = np.zeros((S, T), np.float32)
-    t0 = time.perf_counter()
-    pairs_s = oracle.masked_block_attention(q, k, v, act, skip_bits[0].astype(np.uint8), T, T,
-                                            1 / np.sqrt(T), out)
-    t_attn = time.perf_counter() - t0
-    pairs_all = int(sum(skip_bits[h][cache_bits[h]].sum() for h in range(H)))
-    x = rng.standard_normal((S, dm)).astype(np.float32)
-    wq = (rng.standard_normal((1, dm, T)) * dm ** -0.5).astype(np.float32)
-    nw = np.ones((1, T), np.float32)
-    sel = np.zeros((1, t), bool)
-    sel[0, blocks] = True
-    t0 = time.perf_counter()
-    oracle.project_q(x, wq, nw, sel, T)
-    t_q = time.perf_counter() - t0
-    rows_all = int(cache_bits.sum()) * T
-    # GEMM-O dispatch on the sample row blocks (all heads)
-    o = rng.standard_normal((H, len(blocks) * T, T)).astype(np.float32)
-    w_out = (rng.standard_normal((H, T, dm)) * T ** -0.5).astype(np.float32)
-    active = cache_bits[:, blocks].T
-    bias = [rng.standard_normal((2, T, dm)).astype(np.float32) for _ in blocks]
-    orders = np.where((~active).any(axis=1), 2, 0)
-    t0 = time.perf_counter()
-    oracle.project_out_dispatch(o, w_out, active, bias, orders, 1, 6, 1, T)
-    t_o = time.perf_counter() - t0
-    act_all = int(cache_bits.sum())
-    est = (t_attn * pairs_all / pairs_s + t_q * rows_all / (len(blocks) * T)
-           + t_o * act_all / max(int(active.sum()), 1))
-    sample = (f"{len(blocks)} active q-blocks of head 0 (attention {pairs_s} of {pairs_all} pairs, "
-              f"GEMM-Q), GEMM-O dispatch on those {len(blocks)} row blocks x {H} heads; "
-              f"scaled by exact pair / MAC counts to one full layer step")
-    return est * 1e3, sample, {"attn_ms": t_attn * pairs_all / pairs_s * 1e3,
-                               "gemm_q_ms": t_q * rows_all / (len(blocks) * T) * 1e3,
-                               "gemm_o_ms": t_o * act_all / max(int(active.sum()), 1) * 1e3}
+    return CpuLayer(cfg["seq"], cfg["heads"], cfg["d_model"], cache_bits, skip_bits,
+                    seed=args.seed, order=args.order, elapsed=args.elapsed,
+                    interval=args.interval)
+
+
+def cpu_baseline(args, cfg, cache_bits, skip_bits, k=16):
+    """Bounded sample for the B200 arm's line: slice 0 of a k-way interleaved
+    partition of the layer (1/k of every head's active query blocks, 1/k of
+    the GEMM tiles), scaled to the full layer by exact pair counts (attention)
+    and by k (GEMMs)."""
+    L = cpu_layer(args, cfg, cache_bits, skip_bits)
+    try:
+        L.run_slice(1, 256)  # warm the pool and the BLAS threads
+        sec, parts, pairs = L.run_slice(0, k)
+    finally:
+        L.close()
+    pairs_all = int(L.pairs_per_unit.sum())
+    scale_attn = pairs_all / max(pairs, 1)
+    full = {"attention": parts["attention"] * scale_attn * 1e3,
+            "gemm_q": parts["gemm_q"] * k * 1e3, "gemm_o_dispatch": parts["gemm_o_dispatch"] * k * 1e3}
+    sample = (f"1/{k} of the layer ({pairs} of {pairs_all} attention pairs, every {k}th active "
+              f"(head, q-block) unit; 1/{k} of the GEMM-Q tiles and GEMM-O row blocks), "
+              f"{sec:.1f} s measured, scaled to one full layer step by exact pair counts / {k}; "
+              f"attention backend {L.backend} on {L.workers} worker processes")
+    return sum(full.values()), sample, full, L
 
 
 def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-
-        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
-        if n:
-            return int(max(n))
-    except Exception:
-        pass
     return os.cpu_count()
 
 
 def run_reference(args, cfg, rank, world):
+    """Reference arm: the reference CPU path on the host cores, rank 0 only.
+    The K timed steps are the K slices of an interleaved partition of one
+    layer step, so together they run the WHOLE layer exactly once; the value
+    is their summed time (a measured full layer, not an extrapolation)."""
     if rank != 0:
         return
     rng = np.random.default_rng(args.seed)
     t = cfg["seq"] // T
     cache_bits, skip_bits = random_masks(rng, cfg["heads"], t, args.cached, args.skip)
-    for _ in range(args.warmup):
-        cpu_sample(cfg, cache_bits, skip_bits, args.seed, n_blocks=8)
-    vals = []
-    for s in range(args.steps):
-        ms, sample, parts = cpu_sample(cfg, cache_bits, skip_bits, args.seed + s, n_blocks=8)
-        vals.append(ms)
-    v = float(np.mean(vals))
+    L = cpu_layer(args, cfg, cache_bits, skip_bits)
+    try:
+        for w in range(args.warmup):  # untimed: small slices of a 256-way partition
+            L.run_slice(w, 256)
+        total, parts_sum, pairs = 0.0, {}, 0
+        for s in range(args.steps):
+            sec, parts, p = L.run_slice(s, args.steps)
+            total += sec
+            pairs += p
+            for k2, v2 in parts.items():
+                parts_sum[k2] = parts_sum.get(k2, 0.0) + v2
+    finally:
+        L.close()
+    v = total * 1e3
+    assert pairs == int(L.pairs_per_unit.sum()), "the K slices must cover the layer exactly once"
+    sample = (f"the whole layer step, as {args.steps} interleaved slices (one per timed step; "
+              f"{pairs} attention pairs, all GEMM-Q tiles and GEMM-O row blocks); attention "
+              f"backend {L.backend} on {L.workers} worker processes, GEMMs numpy/OpenBLAS")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1) tensors, random symbols)",
             "config": config_json(args, cfg, world, cache_bits, skip_bits),
-            "breakdown_ms": {k: round(x, 3) for k, x in parts.items()},
+            "breakdown_ms": {k: round(x * 1e3, 3) for k, x in parts_sum.items()},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_threads(),
-                             "kind": "port", "sample": sample.replace("24 active", "8 active")},
+                             "kind": L.kind, "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -400,14 +390,12 @@ def run_b200(args, cfg, rank, world):
     burst, sustained, hbm, src = peaks()
     computed = int(sum(skip_bits[h][cache_bits[h]].sum() for h in heads))
     attn_flops = 4.0 * T * T * T * computed
+    # Q of active tiles, K and V of every (head, block), O of active tiles (bf16)
+    attn_bytes = 2.0 * T * T * (2 * int(cache_bits[heads].sum()) + 2 * Hl * t)
     ach = attn_flops / (parts[1] * 1e-3) / 1e12
-    prof = ROOT / "profiles" / "ncu_r01_summary.json"
-    traffic = None
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get("attention", {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    kname = ("sparse_attention_kernel" if os.environ.get("FO_ATTN_IMPL") == "v1"
+             else "sparse_attention_cs_kernel")
+    traffic, traffic_src = ncu_traffic(kname, args)
     q_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
     o_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
     line = {
@@ -422,12 +410,15 @@ def run_b200(args, cfg, rank, world):
                              "attention": round(ach, 1),
                              "gemm_o_dispatch": round(o_flops / parts[2] / 1e9, 1)},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": sustained,
-                     "unit": "TFLOP/s", "frac": round(ach / sustained, 4), "traffic": traffic,
-                     "kernel": ("sparse_attention_kernel" if os.environ.get("FO_ATTN_IMPL") == "v1"
-                                else "sparse_attention_cs_kernel"),
-                     "peak_source": f"{src} bf16 sustained",
-                     "algorithmic_flops_per_launch": attn_flops},
+        # the timed region is ~0.1 s of back-to-back steps: the burst peak
+        # applies (B200_PROFILING.md); the sustained-peak fraction is beside it
+        "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": burst,
+                     "unit": "TFLOP/s", "frac": round(ach / burst, 4), "traffic": traffic,
+                     "traffic_source": traffic_src, "kernel": kname,
+                     "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                     "peak_sustained": sustained, "frac_sustained": round(ach / sustained, 4),
+                     "algorithmic_flops_per_launch": attn_flops,
+                     "algorithmic_hbm_bytes_per_launch": attn_bytes},
     }
     if "dense_ms" in res:
         dp = res["dense_parts"]
@@ -452,11 +443,31 @@ def run_b200(args, cfg, rank, world):
     if e2e is not None:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu:
-        cms, sample, cparts = cpu_sample(cfg, cache_bits, skip_bits, args.seed)
+        cms, sample, cparts, L = cpu_baseline(args, cfg, cache_bits, skip_bits)
         line["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "cores": cpu_threads(),
-                                "kind": "port", "sample": sample,
+                                "kind": L.kind, "sample": sample,
                                 "breakdown_ms": {k2: round(v2, 1) for k2, v2 in cparts.items()}}
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(kernel, args):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary of the
+    current kernels (profiles/ncu_current.json, written by
+    tools/ncu_summary.py from a --set full capture of this bench's default
+    workload). None when no capture of that kernel at this workload exists."""
+    p = ROOT / "profiles" / "ncu_current.json"
+    if not p.exists():
+        return None, None
+    try:
+        d = json.loads(p.read_text())
+        k = d["kernels"][kernel]
+        w = d.get("workload", {})
+        if (w.get("cached") not in (None, args.cached) or w.get("skip") not in (None, args.skip)
+                or w.get("config", "c4") != args.config):
+            return None, None
+        return float(k["dram_bytes_per_launch"]), f"profiles/{d.get('source', 'ncu_current.json')}"
+    except Exception:
+        return None, None
 
 
 class _Null:

@@ -60,6 +60,9 @@ enum {
 FO_API int fo_abi_version(void);
 FO_API const char* fo_last_error(void);
 FO_API int fo_num_sms(void);
+/* Kernels this library has launched since load (every <<<>>> / cudaLaunchKernelEx
+ * site counts one): the bench's gpu_launches figure. */
+FO_API long long fo_kernel_launches(void);
 
 /* Schedule workspace for one layer's symbols (plan): byte size and the byte
  * offsets of {counts, items, gemm-q tiles, head masks, orders, pairs, gemm-q head-pair jobs}. */

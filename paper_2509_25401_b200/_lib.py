@@ -30,6 +30,7 @@ SIGNATURES = {
     "fo_abi_version": [],
     "fo_last_error": [],
     "fo_num_sms": [],
+    "fo_kernel_launches": [],
     "fo_plan_workspace_bytes": [_I, _I],
     "fo_plan_offsets": [_I, _I, _P],
     "fo_plan_schedule_offset": [_I, _I],
@@ -53,7 +54,7 @@ SIGNATURES = {
 }
 _RESTYPES = {"fo_last_error": ctypes.c_char_p, "fo_plan_workspace_bytes": _SZ,
              "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ,
-             "fo_plan_schedule_offset": _SZ}
+             "fo_plan_schedule_offset": _SZ, "fo_kernel_launches": ctypes.c_longlong}
 
 # return codes / status bits (flashomni_b200.h)
 _CODE_ERRORS = {1: ShapeError, 2: ParameterError, 3: BoundsError, 4: ConsistencyError,
@@ -62,22 +63,17 @@ ST_CONSISTENCY, ST_STATE, ST_BOUNDS, ST_PARAM, ST_TIMEOUT = 0x1, 0x2, 0x4, 0x8, 
 
 _lib = None
 
-# entry point -> kernels it launches (gpu_launches accounting)
-LAUNCHING = {n: 1 for n in ("fo_encode_symbols", "fo_decode_symbols", "fo_plan",
-                            "fo_sparse_attention", "fo_sparse_attention_reuse",
-                            "fo_forecast_materialize", "fo_cache_push",
-                            "fo_gemm_q", "fo_gemm_o_update", "fo_gemm_o_dispatch",
-                            "fo_check_active_match", "fo_synthetic_x", "fo_check_finite")}
-LAUNCHING["fo_generate_masks"] = 5  # pool q, pool k, scores, cache select, skip select
-_launches = [0]
+# kernel launches are counted inside the library (fo_kernel_launches): every
+# launch site in csrc/ bumps one counter, so multi-kernel entry points count exactly
+_launch_base = [0]
 
 
 def reset_launch_count():
-    _launches[0] = 0
+    _launch_base[0] = int(load().fo_kernel_launches())
 
 
 def launch_count():
-    return _launches[0]
+    return int(load().fo_kernel_launches()) - _launch_base[0]
 
 
 def load():
@@ -107,8 +103,6 @@ def call(name, *args):
     reference exception class."""
     lib = load()
     rc = getattr(lib, name)(*args)
-    if name in LAUNCHING and rc == 0:
-        _launches[0] += LAUNCHING[name]
     if rc:
         msg = lib.fo_last_error().decode(errors="replace")
         raise _CODE_ERRORS.get(rc, DeviceError)(f"{name}: {msg}")

@@ -514,6 +514,7 @@ void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtens
                          attn::SMEM_BYTES);
     configured = true;
   }
+  note_launch();
   sparse_attention_kernel<<<grid, attn::NTHREADS, attn::SMEM_BYTES, stream>>>(qm, km, vm, p);
 }
 

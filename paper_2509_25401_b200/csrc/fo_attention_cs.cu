@@ -698,6 +698,7 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
                          attn_cs::SMEM_BYTES);
     configured = true;
   }
+  note_launch();
   sparse_attention_cs_kernel<<<grid, attn_cs::NTHREADS, attn_cs::SMEM_BYTES, stream>>>(qm, km, vm,
                                                                                      p);
 }

@@ -2,6 +2,7 @@
 // construction and kernel launches. No allocation, no synchronisation.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -11,6 +12,11 @@
 #include "fo_internal.cuh"
 
 using namespace fo;
+
+namespace fo {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fo
 
 namespace {
 thread_local char g_err[512] = "";
@@ -140,6 +146,8 @@ extern "C" __attribute__((visibility("default"))) int fo_debug_timing(long long*
 
 extern "C" {
 
+long long fo_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
 int fo_abi_version(void) { return 1; }
 const char* fo_last_error(void) { return g_err; }
 int fo_num_sms(void) { return num_sms(); }
@@ -173,6 +181,7 @@ int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int h
   const long long warps = (long long)heads * (comp_rows + 1);
   const int threads = 256;
   const long long blocks = (warps * 32 + threads - 1) / threads;
+  note_launch();
   encode_symbols_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
       cache_bits, skip_bits, heads, rows, cols, pool_n, s_c, s_s, status);
   return check_launch("encode_symbols");
@@ -184,6 +193,7 @@ int fo_decode_symbols(const uint8_t* s_c, const uint8_t* s_s, int heads, int row
   if (rc) return rc;
   const long long total = (long long)heads * rows * cols;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  note_launch();
   decode_symbols_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols,
                                                                   pool_n, active, pair_bits);
   return check_launch("decode_symbols");
@@ -208,6 +218,7 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
   }
   // heads (2p, 2p+1) active together go to the CTA-pair GEMM-Q (block index < 4096)
   const int gq_pair_heads = !dense && heads % 2 == 0 && rows < 4096 && gemm_2sm_enabled();
+  note_launch();
   plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
                                                        valid, order_d, num_sms(), gq_pair_heads, pv,
                                                        status);
@@ -492,6 +503,7 @@ int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads,
   int rc = check_symbol_dims(heads, rows, 1, pool_n);
   if (rc) return rc;
   const int total = heads * rows;
+  note_launch();
   compare_active_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(s_c_a, s_c_b, heads,
                                                                               rows, pool_n, status);
   return check_launch("check_active_match");

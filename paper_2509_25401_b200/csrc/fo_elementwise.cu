@@ -146,24 +146,28 @@ __global__ void check_finite_kernel(const uint4* __restrict__ data, long long ro
 
 void launch_check_finite(const void* data, long long rows, int cols,
                          const unsigned long long* hmask, uint32_t* status, cudaStream_t stream) {
+  note_launch();
   check_finite_kernel<<<148 * 8, 256, 0, stream>>>(static_cast<const uint4*>(data), rows, cols,
                                                    hmask, status);
 }
 
 void launch_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
                         float c1, float c2, float s, __nv_bfloat16* out, cudaStream_t stream) {
+  note_launch();
   synthetic_x_kernel<<<148 * 8, 256, 0, stream>>>(x0, a, b, n, kind, c1, c2, s, out);
 }
 
 void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,
                                  const unsigned long long* hmask, const int32_t* valid,
                                  const float* coef, __nv_bfloat16* out, cudaStream_t stream) {
+  note_launch();
   forecast_materialize_kernel<<<H * t_q, 256, 0, stream>>>(cache, S, H, t_q, order_d, hmask, valid,
                                                            coef[0], coef[1], coef[2], coef[3], out);
 }
 
 void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,
                        int t_q, int order_d, const uint8_t* sel, cudaStream_t stream) {
+  note_launch();
   cache_push_kernel<<<H * t_q, 256, 0, stream>>>(o, cache, valid, S, H, t_q, order_d, sel);
 }
 

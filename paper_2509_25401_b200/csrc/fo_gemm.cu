@@ -148,6 +148,7 @@ static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaS
     *grid_cache = 2 * std::min(clusters, sms / 2);
   }
   cfg.gridDim = dim3(*grid_cache);
+  note_launch();
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
@@ -993,6 +994,7 @@ void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorM
     configured = true;
   }
   if (p.update) {
+    note_launch();
     gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, om, p);
   } else {
     static int grid_d = 0;

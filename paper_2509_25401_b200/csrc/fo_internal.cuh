@@ -4,6 +4,9 @@
 
 namespace fo {
 
+// counts every kernel launch the library makes (fo_kernel_launches in the C ABI)
+void note_launch();
+
 __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) / b; }
 
 // Per-layer schedule derived from the symbols (built by plan_kernel).

@@ -416,10 +416,12 @@ cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k
   uint8_t* cc = reinterpret_cast<uint8_t*>(w);
 
   const int n_pool = H * rows_c * (kTile / 2);
+  note_launch();
   pool_kernel<<<dim3((n_pool + 255) / 256, 2), 256, 0, stream>>>(q, k, S, H, block, rows_c, pq, pk);
   const size_t sm_sc = scores_smem_bytes(rows_c);
   cudaFuncSetAttribute(scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc);
   const int rows_cta = kScWarps * kScRows;
+  note_launch();
   scores_kernel<<<dim3((rows_c + rows_cta - 1) / rows_cta, H), kScWarps * 32, sm_sc, stream>>>(
       pq, pk, rows_c, pt);
   const int grid_rows = (H * rows_c + kPolWarps - 1) / kPolWarps;
@@ -428,8 +430,10 @@ cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k
       (size_t)rows_c * (3 * sizeof(double) + sizeof(int) + 2) + 8 + (size_t)rows_c * (8 + 4 + 4 + 4);
   cudaFuncSetAttribute(cache_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm_cache);
+  note_launch();
   cache_select_kernel<<<H, 256, sm_cache, stream>>>(pt, rows_c, n_t, tau_q, s_q, cc);
   cudaFuncSetAttribute(skip_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rows);
+  note_launch();
   skip_select_kernel<<<grid_rows, kPolWarps * 32, sm_rows, stream>>>(
       pt, cc, H, rows_c, n_t, tau_kv, guard, pool_n, t_q, cache_bits, skip_bits);
   return cudaGetLastError();

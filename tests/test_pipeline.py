@@ -96,5 +96,7 @@ def test_bench_reference_arm_contract():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "config", "cpu_baseline", "e2e"):
         assert key in line, key
-    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] in ("reference", "port")
+    # one step = the whole layer (the K slices partition it)
+    assert "the whole layer step" in line["cpu_baseline"]["sample"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0

@@ -1,6 +1,11 @@
 """Summarise ncu reports (run here, no GPU): key metrics per kernel -> JSON.
 
     python tools/ncu_summary.py out.json name=gpurun_out/x.ncu-rep [...] [--launches csv]
+        [--current '{"config": "c4", "cached": 0.25, "skip": 0.5}']
+
+--current also writes profiles/ncu_current.json: per kernel (short name) the
+DRAM bytes per launch of these captures, which bench.py reports as
+roofline.traffic when its workload matches.
 """
 
 import csv
@@ -48,6 +53,11 @@ def main():
     res = {}
     launches = None
     args = sys.argv[2:]
+    current = None
+    if "--current" in args:
+        k = args.index("--current")
+        current = json.loads(args[k + 1])
+        args = args[:k] + args[k + 2:]
     if "--launches" in args:
         k = args.index("--launches")
         launches = args[k + 1]
@@ -83,6 +93,18 @@ def main():
                                   "share_of_engine": round(v[1] / tot, 4) if "fo::" in k else None}
                               for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])}
     json.dump(res, open(out_path, "w"), indent=1)
+    if current is not None:
+        import pathlib
+
+        kern = {}
+        for name, d in res.items():
+            if name == "launch_list" or "dram_read_bytes" not in d:
+                continue
+            short = d["kernel"].split("(")[0].split("<")[0].split("::")[-1].strip()
+            kern[short] = {"dram_bytes_per_launch": d["dram_read_bytes"] + d.get("dram_write_bytes", 0),
+                           "capture": name, "report": d["report"]}
+        cur = {"source": pathlib.Path(out_path).name, "workload": current, "kernels": kern}
+        pathlib.Path(out_path).with_name("ncu_current.json").write_text(json.dumps(cur, indent=1))
     print(json.dumps(res, indent=1))
 
 
