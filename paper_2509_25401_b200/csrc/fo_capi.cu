@@ -84,16 +84,6 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
 // Attention kernel: the column-split softmax kernel (fo_attention_cs.cu) by
 // default; FO_ATTN_IMPL=v1 selects the single-warpgroup one (read once per
 // process; both meet the same parity tests)
-// Dense GEMM-Q on CTA pairs (cta_group::2); FO_GEMM_2SM=0 selects the 1-CTA kernel.
-bool gemm_2sm_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FO_GEMM_2SM");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 int attention_impl() {
   static int impl = -1;
   if (impl < 0) {
@@ -169,7 +159,7 @@ void fo_plan_offsets(int heads, int rows, size_t offsets[7]) {
   offsets[3] = reinterpret_cast<size_t>(pv.hmask);
   offsets[4] = reinterpret_cast<size_t>(pv.orders);
   offsets[5] = reinterpret_cast<size_t>(pv.pairs_pred);
-  offsets[6] = reinterpret_cast<size_t>(pv.gq_pairs);
+  offsets[6] = reinterpret_cast<size_t>(pv.gq_jobs);
 }
 
 int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int heads, int rows,
@@ -216,12 +206,10 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
-  // heads (2p, 2p+1) active together go to the CTA-pair GEMM-Q (block index < 4096)
-  const int gq_pair_heads = !dense && heads % 2 == 0 && rows < 4096 && gemm_2sm_enabled();
+  if (rows > 65535) return fail(FO_ERR_PARAM, "too many query blocks for the plan (%d)", rows);
   note_launch();
   plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
-                                                       valid, order_d, num_sms(), gq_pair_heads, pv,
-                                                       status);
+                                                       valid, order_d, num_sms(), pv, status);
   return check_launch("plan");
 }
 
@@ -377,10 +365,10 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   if ((rc = check_align32(q_out, "q_out"))) return rc;
   if (heads < 1 || heads > 64) return fail(FO_ERR_PARAM, "heads must be in [1, 64]");
   if (!dense && !plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
-  CUtensorMap xm, wm;
-  // x moves in half tiles (64 rows), each multicast to both CTAs of a cluster
-  if ((rc = make_map(&xm, x, seq, d_model, 64, "x"))) return rc;
+  CUtensorMap xm, wm, wm64;
+  if ((rc = make_map(&xm, x, seq, d_model, 128, "x"))) return rc;
   if ((rc = make_map(&wm, w_qt, (uint64_t)heads * kTile, d_model, 128, "w_q"))) return rc;
+  if ((rc = make_map(&wm64, w_qt, (uint64_t)heads * kTile, d_model, 64, "w_q"))) return rc;
   const int t_q = ceil_div_d(seq, kTile);
   GemmQParams p;
   p.S = seq;
@@ -388,37 +376,21 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   p.H = heads;
   p.t_q = t_q;
   p.dense = dense;
-  if (plan_ws) {
+  if (!dense) {
     PlanView pv = plan_view(plan_ws, heads, t_q);
-    p.gq_pairs = pv.gq_pairs;
-    p.gq_cjobs = pv.gq_cjobs;
-    p.gq_cjobs2 = pv.gq_cjobs2;
-    p.n_gqc = pv.counts + 5;
-    p.gq2_jobs = pv.gq2_jobs;
-    p.n_gq2 = pv.counts + 7;
+    p.jobs = pv.gq_jobs;
+    p.n_jobs = pv.counts + 7;
   } else {
-    p.gq_pairs = nullptr;
-    p.gq_cjobs = nullptr;
-    p.gq_cjobs2 = nullptr;
-    p.gq2_jobs = nullptr;
-    p.n_gq2 = nullptr;
-    p.n_gqc = nullptr;
+    p.jobs = nullptr;
+    p.n_jobs = nullptr;
   }
   p.norm_w = norm_w;
   p.rope_cos = rope_cos;
   p.rope_sin = rope_sin;
   p.eps = eps;
   p.q = static_cast<__nv_bfloat16*>(q_out);
-  // CTA pairs: every tile of the dense phase; in the sparse phase the blocks
-  // where both heads of a pair (2p, 2p+1) are active (the plan's gq2 jobs, same
-  // rule as fo_plan), then the remaining tiles on the 1-CTA kernel
-  const bool pairs = heads % 2 == 0 && gemm_2sm_enabled() && (dense || t_q < 4096);
-  if (pairs) {
-    CUtensorMap xm2;  // full 128-row x tiles (no multicast on the CTA-pair path)
-    if ((rc = make_map(&xm2, x, seq, d_model, 128, "x"))) return rc;
-    launch_gemm_q2(xm2, wm, p, (cudaStream_t)stream);
-  }
-  if (!(pairs && dense)) launch_gemm_q(xm, wm, p, (cudaStream_t)stream);
+  // one persistent launch on CTA pairs for both phases (fo_gemm.cu gemm_q2_kernel)
+  launch_gemm_q2(xm, wm, wm64, p, (cudaStream_t)stream);
   return check_launch("gemm_q");
 }
 
@@ -490,7 +462,8 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
   if ((rc = make_map_ex(&bm, bias, (uint64_t)(order_d + 1) * seq, d_model, 32, 128,
                         CU_TENSOR_MAP_SWIZZLE_64B, "bias")))
     return rc;
-  if ((rc = make_map_ex(&om, out, seq, d_model, 32, 128, CU_TENSOR_MAP_SWIZZLE_64B, "out")))
+  // output: one 32-row x 32-column box per epilogue warp and chunk
+  if ((rc = make_map_ex(&om, out, seq, d_model, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, "out")))
     return rc;
   // o moves in half tiles (64 rows), each multicast to both CTAs of a cluster
   if ((rc = make_map(&am, o, seq, (uint64_t)heads * kTile, 64, "o"))) return rc;

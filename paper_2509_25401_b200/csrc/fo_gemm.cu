@@ -43,7 +43,7 @@ constexpr int NTHREADS = 256;
 constexpr int D_BN = 256;
 constexpr int D_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
 constexpr int D_STAGES = 3;
-constexpr int BIAS_SLOTS = 4;
+constexpr int BIAS_SLOTS = 8;  // max slots (8 x 8 KB at order 0, 4 x 16 KB at orders >= 1)
 constexpr int BIAS_ORDER_BYTES = BM * 32 * 2;  // 8 KB
 constexpr int BIAS_SLOT_BYTES = 2 * BIAS_ORDER_BYTES;
 
@@ -57,7 +57,8 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
 // output chunks are staged separately (double-buffered) so a bias slot is free
 // as soon as the epilogue has read it, not when the chunk's store has read it
 constexpr int OUT_STAGE_BYTES = BM * 32 * 2;  // 8 KB, SW64 like the bias chunks
-constexpr int SMEM_BYTES_D = D_STAGES * D_STAGE_BYTES + BIAS_SLOTS * BIAS_SLOT_BYTES +
+constexpr int BIAS_RING_BYTES = 4 * BIAS_SLOT_BYTES;  // 64 KB
+constexpr int SMEM_BYTES_D = D_STAGES * D_STAGE_BYTES + BIAS_RING_BYTES +
                              2 * OUT_STAGE_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
@@ -86,6 +87,18 @@ struct Ring {
   int s = 0, ph = 0;
   __device__ __forceinline__ void next() {
     if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+};
+
+// ring cursor over a runtime slot count
+struct DynRing {
+  int s = 0, ph = 0, n;
+  __device__ explicit DynRing(int n_) : n(n_) {}
+  __device__ __forceinline__ void next() {
+    if (++s == n) {
       s = 0;
       ph ^= 1;
     }
@@ -153,24 +166,13 @@ static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaS
 }
 
 // =============================================================================
-// GEMM-Q
+// GEMM-Q: output tile = (query block i, head h), 128 x 128, so RMSNorm over the
+// head dim and RoPE are tile-local; each head's 128 accumulator columns get
+// them in the epilogue. The kernel (gemm_q2_kernel below) runs on CTA pairs.
 // =============================================================================
-// Job = query block i x up to two heads (the plan pairs block i's active heads
-// in order): one 128 x 256 tcgen05 tile (128 x 128 for an odd head out). N=256
-// cuts the operand feed per MMA cycle from 128 to 96 B/SM (A is shared by the
-// two heads). CTAs run in 2-CTA clusters that take two jobs of the same block:
-// each CTA loads half of the x tile and multicasts it to both, cutting the
-// L2 -> SM feed to 80 B per MMA cycle (the mainloop is feed-bound: ncu shows
-// the producer waiting on free stages while the MMA warp waits on data). Each
-// head's 128 accumulator columns get RMSNorm + RoPE in the epilogue.
 namespace gemm {
 constexpr int Q_BN = 256;
-constexpr int Q_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
-constexpr int Q_STAGES = 4;
 constexpr int Q_NW_BYTES = 64 * 128 * 4;  // RMSNorm weights of up to 64 heads
-constexpr int Q_SMEM_BYTES = Q_STAGES * Q_STAGE_BYTES + 1024 + 1024 + Q_NW_BYTES;
-constexpr int A_HALF_BYTES = A_BYTES / 2;  // 64 rows x 64 K, SW128
-static_assert(Q_SMEM_BYTES <= 232448, "GEMM-Q shared memory over the sm_100 limit");
 }  // namespace gemm
 
 namespace gemm {
@@ -277,172 +279,21 @@ __device__ __forceinline__ void q_epilogue_job(const GemmQParams& p, uint32_t ta
 }
 }  // namespace gemm
 
-__global__ void __launch_bounds__(gemm::NTHREADS, 1)
-    gemm_q_kernel(const __grid_constant__ CUtensorMap xm,  // x, box 64 K x 64 rows (half tile)
-                  const __grid_constant__ CUtensorMap wm, const GemmQParams p) {
-  using namespace gemm;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  Bars* bars = reinterpret_cast<Bars*>(smem + Q_STAGES * Q_STAGE_BYTES);
-  float* nw_smem = reinterpret_cast<float*>(smem + Q_STAGES * Q_STAGE_BYTES + 1024);
-  const int warp = warp_id(), lane = lane_id();
-  const int rank = (int)cluster_ctarank();
-  if (p.norm_w)  // RMSNorm weights of every head, read by the epilogue as broadcasts
-    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
-      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
-  if (warp == 0 && lane == 0) {
-    init_bars(bars, 2);
-    tma_prefetch_desc(&xm);
-    tma_prefetch_desc(&wm);
-  }
-  if (warp == 2) tmem_alloc<512>(&bars->tmem_base);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();  // both CTAs' barriers exist before any multicast lands
-  tc_fence_after();
-  const uint32_t tbase = bars->tmem_base;
-  const int nph = (p.H + 1) >> 1;  // head pairs per block (dense phase)
-  const int ncp = (nph + 1) >> 1;  // cluster jobs per block (dense phase)
-  const int n_cjobs = p.dense ? p.t_q * ncp : *p.n_gqc;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int nkb = p.dm / BK;
-  // cluster job -> (block i, this CTA's heads h1/h2); false: no job for this CTA
-  // (it still releases the stages in step with its partner). shared: both CTAs
-  // work on the same block, each loads half of the x tile and multicasts it;
-  // otherwise each loads its own x tile.
-  auto job = [&](int c, int& i, int& h1, int& h2, bool& shared) -> bool {
-    if (p.dense) {
-      i = c / ncp;
-      const int pp = 2 * (c - i * ncp) + rank;
-      h1 = 2 * pp;
-      h2 = (h1 + 1 < p.H) ? h1 + 1 : -1;
-      shared = 2 * (c - i * ncp) + 1 < nph;
-      return pp < nph;
-    }
-    const int j0 = p.gq_cjobs[c], j1 = p.gq_cjobs2[c];
-    const int c0 = p.gq_pairs[j0];
-    const int c1 = j1 >= 0 ? p.gq_pairs[j1] : c0;
-    shared = j1 >= 0 && (c0 & 0xFFFF) == (c1 & 0xFFFF);
-    const int code = rank ? c1 : c0;
-    i = code & 0xFFFF;
-    h1 = (code >> 16) & 0xFF;
-    h2 = (code >> 24) - 1;
-    return rank == 0 || j1 >= 0;
-  };
-
-  if (warp == 0) {
-    // TMA producer (whole warp walks the schedule; one elected lane issues)
-    Ring<Q_STAGES> rg;
-    for (int c = cid; c < n_cjobs; c += ncl) {
-      int i, h1, h2;
-      bool shared;
-      const bool mine = job(c, i, h1, h2, shared);
-      const uint32_t bytes = mine ? A_BYTES + (h2 >= 0 ? 2 : 1) * B_BYTES : 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
-        if (elect_one()) {
-          uint8_t* st = smem + rg.s * Q_STAGE_BYTES;
-          mbar_arrive_expect_tx(&bars->full[rg.s], bytes);
-          if (shared) {
-            tma_load_2d_mc(st + rank * A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK,
-                           i * BM + rank * (BM / 2), 0x3);
-          } else if (mine) {
-            tma_load_2d(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
-            tma_load_2d(st + A_HALF_BYTES, &xm, &bars->full[rg.s], kb * BK, i * BM + BM / 2);
-          }
-          if (mine) {
-            tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, h1 * BN);
-            if (h2 >= 0)
-              tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], kb * BK, h2 * BN);
-          }
-        }
-        __syncwarp();
-        rg.next();
-      }
-    }
-    // drain: every stage released by both CTAs' MMA warps, so no arrival from the
-    // peer can target this CTA after it leaves the final cluster barrier
-    for (int k = 0; k < Q_STAGES; ++k) {
-      mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
-      rg.next();
-    }
-  } else if (warp == 1) {
-    // MMA issuer (warp-uniform schedule, elected lane issues + commits)
-    const uint32_t idesc2 = make_idesc_bf16(BM, Q_BN, false, false);
-    const uint32_t idesc1 = make_idesc_bf16(BM, BN, false, false);
-    const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
-    Ring<Q_STAGES> rg;
-    int t = 0;
-    for (int c = cid; c < n_cjobs; c += ncl) {
-      int i, h1, h2;
-      bool shared;
-      const bool mine = job(c, i, h1, h2, shared);
-      const uint32_t idesc = h2 >= 0 ? idesc2 : idesc1;
-      const int acc = t & 1;
-      if (mine) {
-        mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
-        tc_fence_after();
-      }
-      const uint32_t d = tbase + acc * Q_BN;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&bars->full[rg.s], rg.ph);
-        tc_fence_after();
-        const uint64_t a = desc0 + (uint64_t)((rg.s * Q_STAGE_BYTES) >> 4);
-        if (elect_one()) {
-          if (mine) mma_kblock(d, a, a + (A_BYTES >> 4), idesc, kb > 0);
-          tc_commit_mc(&bars->empty[rg.s], 0x3);  // the stage is free in both CTAs' view
-        }
-        __syncwarp();
-        rg.next();
-      }
-      if (mine) {
-        if (elect_one()) tc_commit(&bars->tfull[acc]);
-        __syncwarp();
-        ++t;
-      }
-    }
-  } else if (warp >= 4) {
-    // epilogue: one accumulator row per thread. Pass 1 reads both heads' rows
-    // from TMEM for the RMS sums; pass 2 walks 32-column chunks, loading the
-    // row's rotary chunk once for both heads (prefetched a chunk ahead) and
-    // the norm weights from shared memory.
-    const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    const uint32_t nw_u32 = smem_u32(nw_smem);
-    int t = 0;
-    for (int c = cid; c < n_cjobs; c += ncl) {
-      int i, h1, h2;
-      bool shared;
-      if (!job(c, i, h1, h2, shared)) continue;
-      const int acc = t & 1;
-      mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
-      tc_fence_after();
-      ++t;
-      gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, [&]() {
-        tc_fence_before();
-        mbar_arrive(&bars->tempty[acc]);
-      });
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tbase);
-  }
-}
-
 // =============================================================================
-// GEMM-Q dense phase on CTA pairs (cta_group::2): the update-step Q and the K / V
-// projections. A cluster job is two query blocks x two heads, one 256 x 256
-// tcgen05 tile over both SMs: each CTA loads its own 128 x-rows and its own
-// head's 128 W-rows per k-block, and the even CTA issues M=256 / N=256 MMAs that
-// read both CTAs' shared memory and write 128 rows to each CTA's TMEM. The feed
-// is 64 B per MMA cycle per SM (96 for the 1-CTA 128 x 256 tile). Needs an even
-// head count; the plan-driven sparse phase stays on gemm_q_kernel.
+// GEMM-Q on CTA pairs (cta_group::2), every tile of both phases in one
+// persistent launch. A cluster job is two query blocks (i0 on CTA 0, i1 on
+// CTA 1) x one N-tile of heads, one M=256 tcgen05 tile over both SMs:
+//   N=256: heads (h, h+1) active in both blocks; each CTA loads its 128 x rows
+//          and its own head's 128 W rows per k-block (B is split by CTA);
+//   N=128: head h alone; each CTA loads its 128 x rows and 64 of h's W rows.
+// The even CTA issues the MMAs, which read both CTAs' shared memory and write
+// each CTA's 128 accumulator rows to its own TMEM. Per SM the operand feed is
+// 64 B per MMA cycle (N=256) or 96 B (N=128), against 128 B for a 1-CTA
+// 128 x 128 tile. The dense phase walks (block pair, head pair) jobs in place
+// (plus an N=128 job per block pair for an odd last head); the sparse phase
+// walks the plan's job list (PlanView::gq_jobs), which is ordered by first
+// block so jobs in flight share x tiles in L2. A job with one block loads
+// zero rows past the end on CTA 1 (TMA fills them) and skips its epilogue.
 // =============================================================================
 namespace gemm {
 constexpr int Q2_STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KB per CTA
@@ -452,8 +303,10 @@ static_assert(Q2_SMEM_BYTES <= 232448, "2-CTA GEMM-Q shared memory over the sm_1
 }  // namespace gemm
 
 __global__ void __launch_bounds__(gemm::NTHREADS, 1)
-    gemm_q2_kernel(const __grid_constant__ CUtensorMap xm,  // x, box 64 K x 128 rows
-                   const __grid_constant__ CUtensorMap wm, const GemmQParams p) {
+    gemm_q2_kernel(const __grid_constant__ CUtensorMap xm,    // x, box 64 K x 128 rows
+                   const __grid_constant__ CUtensorMap wm,    // W_q, box 64 K x 128 rows
+                   const __grid_constant__ CUtensorMap wm64,  // W_q, box 64 K x 64 rows
+                   const GemmQParams p) {
   using namespace gemm;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -477,6 +330,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     fence_barrier_init();
     tma_prefetch_desc(&xm);
     tma_prefetch_desc(&wm);
+    tma_prefetch_desc(&wm64);
   }
   if (warp == 2) tmem_alloc_2sm<512>(&bars->tmem_base);
   tc_fence_before();
@@ -484,45 +338,52 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
-  const int nph = p.H >> 1;                    // head pairs
-  const int nbp = (p.t_q + 1) >> 1;            // block pairs
-  const int n_cjobs = p.dense ? nbp * nph : *p.n_gq2;
+  const int nph = p.H >> 1;            // full head pairs
+  const int npj = nph + (p.H & 1);     // dense jobs per block pair (odd last head: N=128)
+  const int nbp = (p.t_q + 1) >> 1;    // block pairs
+  const int n_cjobs = p.dense ? nbp * npj : *p.n_jobs;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int nkb = p.dm / BK;
-  // job -> this CTA's block i and heads (h1, h2); false: no block for this CTA
-  // (a sparse job with one block: the CTA loads zero rows past the end and
-  // skips its epilogue)
-  auto job = [&](int c, int& i, int& h1, int& h2) -> bool {
+  // job -> this CTA's block i, head h and width (n256: heads h, h+1); false: no
+  // block for this CTA (it loads zero rows past the end and skips its epilogue)
+  auto job = [&](int c, int& i, int& h, bool& n256) -> bool {
+    int i0, i1;
     if (p.dense) {  // block-pair-major
-      const int bp = c / nph;
-      i = 2 * bp + rank;
-      h1 = 2 * (c - bp * nph);
-      h2 = h1 + 1;
-      return true;
+      const int bp = c / npj, r = c - bp * npj;
+      i0 = 2 * bp;
+      i1 = 2 * bp + 1 < p.t_q ? 2 * bp + 1 : -1;
+      h = 2 * r;
+      n256 = r < nph;
+    } else {
+      const int2 code = p.jobs[c];
+      i0 = code.x & 0xFFFF;
+      i1 = (code.x >> 16) - 1;
+      h = code.y & 0xFF;
+      n256 = (code.y >> 8) & 1;
     }
-    const int code = p.gq2_jobs[c];
-    const int i0 = code & 0xFFF, i1 = ((code >> 12) & 0xFFF) - 1;
-    h1 = 2 * (code >> 24);
-    h2 = h1 + 1;
     i = rank ? (i1 >= 0 ? i1 : p.t_q) : i0;
     return rank == 0 || i1 >= 0;
   };
 
   if (warp == 0) {
-    // both CTAs load their own x rows and their own head's W rows; the bytes
+    // both CTAs load their own x rows and their half of B; the bytes of both
     // land on the even CTA's full barrier
     Ring<Q2_STAGES> rg;
     for (int c = cid; c < n_cjobs; c += ncl) {
-      int i, h1, h2;
-      job(c, i, h1, h2);  // a missing block loads zero rows (coordinates past the end)
-      const int hh = rank ? h2 : h1;
+      int i, h;
+      bool n256;
+      job(c, i, h, n256);  // a missing block loads zero rows (coordinates past the end)
+      const uint32_t b_bytes = n256 ? B_BYTES : B_BYTES / 2;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
           uint8_t* st = smem + rg.s * Q2_STAGE_BYTES;
-          if (rank == 0) mbar_arrive_expect_tx(&bars->full[rg.s], 2 * Q2_STAGE_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(&bars->full[rg.s], 2 * (A_BYTES + b_bytes));
           tma_load_2d_2sm(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
-          tma_load_2d_2sm(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, hh * BN);
+          if (n256)
+            tma_load_2d_2sm(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, (h + rank) * BN);
+          else
+            tma_load_2d_2sm(st + A_BYTES, &wm64, &bars->full[rg.s], kb * BK, h * BN + rank * 64);
         }
         __syncwarp();
         rg.next();
@@ -530,11 +391,16 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     }
   } else if (warp == 1 && rank == 0) {
     // MMA issuer of the pair
-    const uint32_t idesc = make_idesc_bf16(2 * BM, Q_BN, false, false);
+    const uint32_t idesc256 = make_idesc_bf16(2 * BM, Q_BN, false, false);
+    const uint32_t idesc128 = make_idesc_bf16(2 * BM, BN, false, false);
     const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
     Ring<Q2_STAGES> rg;
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl, ++t) {
+      int i, h;
+      bool n256;
+      job(c, i, h, n256);
+      const uint32_t idesc = n256 ? idesc256 : idesc128;
       const int acc = t & 1;
       mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -563,8 +429,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const uint32_t nw_u32 = smem_u32(nw_smem);
     int t = 0;
     for (int c = cid; c < n_cjobs; c += ncl, ++t) {
-      int i, h1, h2;
-      const bool mine = job(c, i, h1, h2);
+      int i, h;
+      bool n256;
+      const bool mine = job(c, i, h, n256);
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -574,7 +441,8 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
         if (lane == 0) mbar_arrive_cluster(&bars->tempty[acc], 0);
       };
       if (mine)
-        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h1, h2, nw_u32, release);
+        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h, n256 ? h + 1 : -1, nw_u32,
+                             release);
       else
         release();
     }
@@ -588,10 +456,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   }
 }
 
-void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
-                    cudaStream_t stream) {
+void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const CUtensorMap& wm64,
+                    const GemmQParams& p, cudaStream_t stream) {
   static int grid = 0;
-  launch_pair_clusters(gemm_q2_kernel, gemm::Q2_SMEM_BYTES, &grid, stream, xm, wm, p);
+  launch_pair_clusters(gemm_q2_kernel, gemm::Q2_SMEM_BYTES, &grid, stream, xm, wm, wm64, p);
 }
 
 // =============================================================================
@@ -626,7 +494,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem + ST * SB;  // dispatch bias / output chunks
-  uint8_t* ostage = ring + (UPDATE ? 0 : BIAS_SLOTS * BIAS_SLOT_BYTES);  // dispatch out chunks
+  uint8_t* ostage = ring + (UPDATE ? 0 : BIAS_RING_BYTES);  // dispatch out chunks
   Bars* bars = reinterpret_cast<Bars*>(ostage + (UPDATE ? 0 : 2 * OUT_STAGE_BYTES));
   const int warp = warp_id(), lane = lane_id();
   const int rank = MC ? (int)cluster_ctarank() : 0;
@@ -674,6 +542,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   // dispatch: bias orders staged through the ring for block i (orders >= 2 are
   // rare and read directly)
   auto staged_orders = [&](int i) { return min(min(p.order_d + 1, p.orders[i]), 2); };
+  // the 64 KB bias ring holds 8 KB per staged order and chunk: 8 slots when
+  // only order 0 is staged (twice the bytes in flight of a fixed 4-slot ring)
+  const int bias_slot_bytes = min(p.order_d + 1, 2) * BIAS_ORDER_BYTES;
+  const int bias_slots = BIAS_RING_BYTES / bias_slot_bytes;
 
   if (warp == 0) {
     {
@@ -777,7 +649,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     __syncwarp();
   } else if (!UPDATE && warp == 3) {
     // bias loader: 4 chunks per job through the slot ring, next job prefetched into L2
-    Ring<BIAS_SLOTS> rb;
+    DynRing rb(bias_slots);
     for (int w = jstart; w < n_jobs; w += jstep) {
       int i, nb, d;
       if (!job(w, i, nb, d)) continue;
@@ -795,7 +667,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&bars->bempty[rb.s], rb.ph ^ 1);
         if (elect_one()) {
-          uint8_t* slot = ring + rb.s * BIAS_SLOT_BYTES;
+          uint8_t* slot = ring + rb.s * bias_slot_bytes;
           mbar_arrive_expect_tx(&bars->bfull[rb.s], ns * BIAS_ORDER_BYTES);
           for (int dd = 0; dd < ns; ++dd)
 #if FO_GO_EVICT_FIRST
@@ -863,7 +735,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       const uint32_t ring_u32 = smem_u32(ring);
       const uint32_t ostage_u32 = smem_u32(ostage);
       const int sw = (r >> 1) & 3;  // SW64: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
-      Ring<BIAS_SLOTS> rb;
+      DynRing rb(bias_slots);
       int ob = 0;  // output staging buffer of this chunk
       int t = 0;
       for (int w = jstart; w < n_jobs; w += jstep) {
@@ -893,79 +765,80 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
             mbar_arrive(&bars->tempty[acc]);
           }
           mbar_wait(&bars->bfull[rb.s], rb.ph);
-          const uint32_t rowa = ring_u32 + rb.s * BIAS_SLOT_BYTES + r * 64;
+          const uint32_t rowa = ring_u32 + rb.s * bias_slot_bytes + r * 64;
+          // every shared-memory load of the chunk first, then packed FMAs
+          uint4 b0[4], b1[4];
+          if (ns > 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b0[q] = lds128(rowa + ((q ^ sw) << 4));
+          }
+          if (ns > 1) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b1[q] = lds128(rowa + BIAS_ORDER_BYTES + ((q ^ sw) << 4));
+          }
+          float2 o2[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            o2[k] = make_float2(__uint_as_float(ua[2 * k]), __uint_as_float(ua[2 * k + 1]));
+          auto fma_bias = [&](const uint4 (&bb)[4], float cf) {
+            const float2 c2v = make_float2(cf, cf);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t w4[4] = {bb[q].x, bb[q].y, bb[q].z, bb[q].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                o2[q * 4 + e] = ffma2(c2v, make_float2(bf16lo(w4[e]), bf16hi(w4[e])), o2[q * 4 + e]);
+            }
+          };
+          if (ns > 0) fma_bias(b0, c0);
+          if (ns > 1) fma_bias(b1, c1);
+          if (no > 2 && row_ok) {  // orders 2..3 (rare): direct loads
+            for (int dd = 2; dd < no; ++dd) {
+              uint4 bb[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                bb[q] = __ldg(reinterpret_cast<const uint4*>(
+                    p.bias + dd * SD + (size_t)row * p.dm + (size_t)nb * TBN + c * 32 + q * 8));
+              fma_bias(bb, dd == 2 ? c2 : c3);
+            }
+          }
           uint4 res[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t a = rowa + ((q ^ sw) << 4);
-            float o[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] = __uint_as_float(ua[q * 8 + k]);
-            if (ns > 0) {
-              const uint4 b = lds128(a);
-              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                o[2 * e] = fmaf(c0, bf16lo(w4[e]), o[2 * e]);
-                o[2 * e + 1] = fmaf(c0, bf16hi(w4[e]), o[2 * e + 1]);
-              }
-            }
-            if (ns > 1) {
-              const uint4 b = lds128(a + BIAS_ORDER_BYTES);
-              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                o[2 * e] = fmaf(c1, bf16lo(w4[e]), o[2 * e]);
-                o[2 * e + 1] = fmaf(c1, bf16hi(w4[e]), o[2 * e + 1]);
-              }
-            }
-            for (int dd = 2; dd < no; ++dd) {  // orders 2..3 (rare): direct loads
-              if (!row_ok) break;
-              const float cf = dd == 2 ? c2 : c3;
-              const uint4 b = __ldg(reinterpret_cast<const uint4*>(
-                  p.bias + dd * SD + (size_t)row * p.dm + (size_t)nb * TBN + c * 32 + q * 8));
-              const uint32_t w4[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                o[2 * e] = fmaf(cf, bf16lo(w4[e]), o[2 * e]);
-                o[2 * e + 1] = fmaf(cf, bf16hi(w4[e]), o[2 * e + 1]);
-              }
-            }
-            res[q] = make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]),
-                                pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
-          }
+          for (int q = 0; q < 4; ++q)
+            res[q] = make_uint4(pack_bf16x2(o2[4 * q].x, o2[4 * q].y),
+                                pack_bf16x2(o2[4 * q + 1].x, o2[4 * q + 1].y),
+                                pack_bf16x2(o2[4 * q + 2].x, o2[4 * q + 2].y),
+                                pack_bf16x2(o2[4 * q + 3].x, o2[4 * q + 3].y));
           __syncwarp();  // this warp's rows of the bias slot are read: release it
           if (lane == 0) mbar_arrive(&bars->bempty[rb.s]);
           rb.next();
-          // the store that last used this staging buffer (two chunks ago) has read
-          // it: the elected thread waited for that before arriving here
-          named_bar_sync(1, 128);
+          // each warp stores its own 32 rows (a 32 x 32 TMA box) from its quarter
+          // of staging buffer ob, so the four epilogue warps never wait for each
+          // other; the store that last read this quarter (two chunks ago) is done
+          // reading (lane 0 waited for it right after issuing the next one)
           const uint32_t orow = ostage_u32 + ob * OUT_STAGE_BYTES + r * 64;
 #pragma unroll
           for (int q = 0; q < 4; ++q) sts128(orow + ((q ^ sw) << 4), res[q]);
           fence_proxy_async();
-          named_bar_sync(1, 128);
-          if (warp == 4) {
-            if (elect_one()) {
+          __syncwarp();
+          if (lane == 0) {
+            uint8_t* src = ostage + ob * OUT_STAGE_BYTES + q4 * (OUT_STAGE_BYTES / 4);
 #if FO_GO_EVICT_FIRST
-              tma_store_2d_hint(&om, ostage + ob * OUT_STAGE_BYTES, nb * TBN + c * 32, i * BM,
-                                l2_evict_first_policy());
+            tma_store_2d_hint(&om, src, nb * TBN + c * 32, i * BM + q4 * 32,
+                              l2_evict_first_policy());
 #else
-              tma_store_2d(&om, ostage + ob * OUT_STAGE_BYTES, nb * TBN + c * 32, i * BM);
+            tma_store_2d(&om, src, nb * TBN + c * 32, i * BM + q4 * 32);
 #endif
-              bulk_commit();
-              bulk_wait_read<1>();  // the other staging buffer's store has read it
-            }
-            __syncwarp();
+            bulk_commit();
+            bulk_wait_read<1>();  // this warp's quarter of the other buffer is free
           }
+          __syncwarp();
           ob ^= 1;
         }
         ++t;
       }
-      if (warp == 4) {
-        if (elect_one()) bulk_wait<0>();
-        __syncwarp();
-      }
+      if (lane == 0) bulk_wait<0>();
+      __syncwarp();
     }
   }
   tc_fence_before();
@@ -975,12 +848,6 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc<TM_COLS>(tbase);
   }
-}
-
-void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
-                   cudaStream_t stream) {
-  static int grid = 0;
-  launch_pair_clusters(gemm_q_kernel, gemm::Q_SMEM_BYTES, &grid, stream, xm, wm, p);
 }
 
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,

@@ -13,26 +13,27 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
                               // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
-                              // [4] GEMM-Q head-pair jobs, [5] GEMM-Q cluster jobs,
+                              // [4], [5] unused,
                               // [6] attention waves of the balanced schedule,
-                              // [7] GEMM-Q CTA-pair jobs
+                              // [7] GEMM-Q jobs (gq_jobs)
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
   int* gq_items;              // [H*rows] GEMM-Q tiles (h<<20)|i in (block, head) order, then
                               // the cached tiles in the same order from index counts[1]
   unsigned long long* hmask;  // [rows] bit h set = head h computed for block i
   int* orders;                // [rows] cached-bias orders per block (0 = no cached heads)
   long long* pairs_pred;      // [H] mask-predicted computed pairs
-  int* gq_pairs;              // [H*rows] GEMM-Q jobs: block i x up to two active heads,
-                              // i | h1 << 16 | (h2 + 1) << 24 (h2 = -1: single head)
-  int* gq_cjobs;              // [H*rows] GEMM-Q jobs of one 2-CTA cluster: rank 0's job index
-  int* gq_cjobs2;             // [H*rows] rank 1's job index (-1: none); same block = shared x
+  int* scratch;               // [H*rows] plan-internal scratch (per-row KV counts)
   int* att_sched;             // [H*rows + 1024] attention item of (wave k, CTA b) at k*P + b, -1 none
-  int* gq2_jobs;              // [H*rows/2 + 64] GEMM-Q CTA-pair jobs: blocks i0, i1 x heads (2p, 2p+1)
-                              // both active; i0 | (i1 + 1) << 12 | p << 24 (i1 = -1: one block)
+  int2* gq_jobs;              // [gq_jobs_cap] GEMM-Q jobs of the CTA-pair kernel (counts[7] of
+                              // them): x = i0 | (i1 + 1) << 16 (query blocks of CTA 0 / 1, i1 = -1:
+                              // none), y = h | n256 << 8 (n256: heads h, h+1 as one N=256 tile,
+                              // else head h alone, N=128); ordered by i0
 };
 
-__host__ __device__ inline int gq_pair_code(int i, int h1, int h2) {
-  return i | (h1 << 16) | ((h2 + 1) << 24);
+// GEMM-Q job capacity: per head pair, three block lists (both heads / only the
+// first / only the second active) cut into jobs of two blocks
+__host__ __device__ inline int gq_jobs_cap(int H, int rows) {
+  return H * rows / 2 + 3 * ((H + 1) / 2) + 64;
 }
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -50,11 +51,9 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
   size_t o_hm = take((size_t)rows * sizeof(unsigned long long));
   size_t o_ord = take((size_t)rows * sizeof(int));
   size_t o_pairs = take((size_t)H * sizeof(long long));
-  size_t o_gqp = take((size_t)H * rows * sizeof(int));
-  size_t o_gqc = take((size_t)H * rows * sizeof(int));
-  size_t o_gqc2 = take((size_t)H * rows * sizeof(int));
+  size_t o_scr = take((size_t)H * rows * sizeof(int));
   size_t o_sched = take(((size_t)H * rows + 1024) * sizeof(int));
-  size_t o_gq2 = take(2 * ((size_t)H * rows / 2 + 64) * sizeof(int));  // + sort scratch
+  size_t o_gq2 = take(2 * (size_t)gq_jobs_cap(H, rows) * sizeof(int2));  // + sort scratch
   if (pv) {
     pv->counts = reinterpret_cast<int*>(base + o_counts);
     pv->items = reinterpret_cast<int2*>(base + o_items);
@@ -62,11 +61,9 @@ inline size_t plan_layout(int H, int rows, char* base, PlanView* pv) {
     pv->hmask = reinterpret_cast<unsigned long long*>(base + o_hm);
     pv->orders = reinterpret_cast<int*>(base + o_ord);
     pv->pairs_pred = reinterpret_cast<long long*>(base + o_pairs);
-    pv->gq_pairs = reinterpret_cast<int*>(base + o_gqp);
-    pv->gq_cjobs = reinterpret_cast<int*>(base + o_gqc);
-    pv->gq_cjobs2 = reinterpret_cast<int*>(base + o_gqc2);
+    pv->scratch = reinterpret_cast<int*>(base + o_scr);
     pv->att_sched = reinterpret_cast<int*>(base + o_sched);
-    pv->gq2_jobs = reinterpret_cast<int*>(base + o_gq2);
+    pv->gq_jobs = reinterpret_cast<int2*>(base + o_gq2);
   }
   return off;
 }
@@ -78,7 +75,7 @@ __global__ void decode_symbols_kernel(const uint8_t* s_c, const uint8_t* s_s, in
                                       int cols, int pool_n, uint8_t* active, uint8_t* pair_bits);
 __global__ void plan_kernel(const uint8_t* s_c, const uint8_t* s_s, int H, int rows, int cols,
                             int pool_n, int dense, const int32_t* valid, int order_d, int ctas,
-                            int gq_pair_heads, PlanView pv, uint32_t* status);
+                            PlanView pv, uint32_t* status);
 __global__ void compare_active_kernel(const uint8_t* s_c_a, const uint8_t* s_c_b, int H, int rows,
                                       int pool_n, uint32_t* status);
 
@@ -192,24 +189,19 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
 // ---------------------------------------------------------------------------
 struct GemmQParams {
   int S, dm, H, t_q, dense;
-  const int* gq_pairs;  // plan head-pair jobs (sparse phase)
-  const int* gq_cjobs;  // plan cluster jobs over gq_pairs (sparse phase): rank 0's job
-  const int* gq_cjobs2;  // rank 1's job (-1: none)
-  const int* gq2_jobs;   // CTA-pair jobs (sparse phase on gemm_q2_kernel)
-  const int* n_gq2;      // their count
-  const int* n_gqc;     // their count
-  const float* norm_w;  // [H, 128]
+  const int2* jobs;       // sparse phase: plan gq_jobs (CTA-pair jobs, see PlanView)
+  const int* n_jobs;      // their count (plan counts[7])
+  const float* norm_w;    // [H, 128]
   const float* rope_cos;  // [S, 64]
   const float* rope_sin;  // [S, 64]
   float eps;
   __nv_bfloat16* q;  // [S, H*128]
 };
-// persistent, one 2-CTA cluster per SM pair (grid from the co-resident cluster count)
-void launch_gemm_q(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
-                   cudaStream_t stream);
-// dense phase on CTA pairs (cta_group::2); xm with a 128-row box, even head count
-void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const GemmQParams& p,
-                    cudaStream_t stream);
+// GEMM-Q on CTA pairs (cta_group::2), persistent: every tile of the dense phase
+// and of the sparse phase in one launch. xm: x with a 128-row box; wm / wm64:
+// W_q with 128- and 64-row boxes (N=256 and N=128 jobs)
+void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const CUtensorMap& wm64,
+                    const GemmQParams& p, cudaStream_t stream);
 
 struct GemmOParams {
   int S, dm, H, t_q, order_d;

@@ -100,7 +100,7 @@ __global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uin
 __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
-            int ctas, int gq_pair_heads, PlanView pv, uint32_t* status) {
+            int ctas, PlanView pv, uint32_t* status) {
   // Attention items are ordered head-major, longest rows first within a head:
   // CTAs stride through the list together, so the K/V of the ~1-2 heads in
   // flight stay L2-resident while per-CTA work stays balanced.
@@ -146,10 +146,10 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     }
     pv.orders[i] = no;
   }
-  // per-(head, block) KV counts, computed once and kept in gq_cjobs2 (free until
-  // pass 4) for pass 2. The row's bytes are loaded 8 at a time before use, so a
+  // per-(head, block) KV counts, computed once and kept in the plan scratch for
+  // pass 2. The row's bytes are loaded 8 at a time before use, so a
   // row costs a few load latencies instead of one per byte.
-  int* kvc = pv.gq_cjobs2;
+  int* kvc = pv.scratch;
   for (int idx = tid; idx < total; idx += nt) {
     const int h = idx / rows, i = idx % rows;
     int c = -1;
@@ -370,170 +370,85 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     pv.counts[2] = 0;  // fused-forecast cursor and CTA count (attention, materialize mode)
     pv.counts[3] = 0;
   }
-  // pass 4: GEMM-Q head-pair jobs. With gq_pair_heads, heads (2p, 2p+1) active
-  // together in a block go to the CTA-pair kernel (pass 5); the rest here.
-  // Block i's remaining active heads are paired in order (an odd one out runs
-  // alone), so every job is one N=256 (or N=128) tile and no skipped tile is
-  // ever computed. Jobs are block-major.
+  // pass 4: GEMM-Q jobs, all for the CTA-pair kernel (one launch). For head
+  // pair p = (2p, 2p+1) (the last head alone when H is odd), the blocks where
+  // both heads are active form N=256 jobs and the blocks where only one is
+  // active N=128 jobs of that head; each of the three lists is cut into jobs
+  // of two blocks (one per CTA; the last may hold one). Every active tile is in
+  // exactly one job and no cached tile is computed. Jobs are then ordered by
+  // first block (counting sort), so the jobs in flight share x tiles in L2.
   __syncthreads();  // pass 3 read scan[]; hmask (pass 1) is visible block-wide
-  // the pair path pays for itself only when it covers most of the work
-  // (measured: +3% at 75% coverage, slower at 50%): two launches and two tails
-  __shared__ int s_pair_tiles;
-  if (tid == 0) s_pair_tiles = 0;
-  __syncthreads();
-  if (gq_pair_heads) {
-    int c = 0;
-    for (int i = tid; i < rows; i += nt) {
-      const unsigned long long m = pv.hmask[i];
-      c += 2 * __popcll(m & (m >> 1) & 0x5555555555555555ull);
-    }
-    atomicAdd(&s_pair_tiles, c);
-  }
-  __syncthreads();
-  const bool use_pairs = gq_pair_heads && (long long)s_pair_tiles * 10 >= (long long)n_active * 7;
-  auto rest_mask = [&](int i) -> unsigned long long {
-    const unsigned long long m = pv.hmask[i];
-    if (!use_pairs) return m;
-    const unsigned long long both = m & (m >> 1) & 0x5555555555555555ull;  // bit 2p: pair p
-    return m & ~(both | (both << 1));
-  };
-  const int per_b = ceil_div_d(rows, nt);
-  const int blo = min(rows, tid * per_b), bhi = min(rows, blo + per_b);
-  int nloc = 0;
-  for (int i = blo; i < bhi; ++i) nloc += (__popcll(rest_mask(i)) + 1) >> 1;
-  scan[tid] = nloc;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    int v = tid >= off ? scan[tid - off] : 0;
-    __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
-  }
-  int jp = scan[tid] - nloc;
-  const int n_jobs_q = scan[nt - 1];
-  __syncthreads();
-  // cluster jobs (one job per CTA of a 2-CTA cluster): first the pairs of jobs
-  // of the same block (they share, and multicast, the x tile), then the blocks'
-  // odd jobs paired across blocks (each CTA loads its own x tile)
-  int floc = 0, sloc = 0;
-  for (int i = blo; i < bhi; ++i) {
-    const int nj = (__popcll(rest_mask(i)) + 1) / 2;
-    floc += nj / 2;
-    sloc += nj & 1;
-  }
-  scan[tid] = floc;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    int v = tid >= off ? scan[tid - off] : 0;
-    __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
-  }
-  int jf = scan[tid] - floc;
-  const int n_full = scan[nt - 1];
-  __syncthreads();
-  scan[tid] = sloc;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {
-    int v = tid >= off ? scan[tid - off] : 0;
-    __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
-  }
-  int js = scan[tid] - sloc;
-  const int n_single = scan[nt - 1];
-  for (int i = blo; i < bhi; ++i) {
-    const int nj = (__popcll(rest_mask(i)) + 1) / 2;
-    for (int k = 0; k + 1 < nj; k += 2) {
-      pv.gq_cjobs[jf] = jp + k;
-      pv.gq_cjobs2[jf++] = jp + k + 1;
-    }
-    if (nj & 1) {
-      const int slot = n_full + (js >> 1);
-      if (js & 1)
-        pv.gq_cjobs2[slot] = jp + nj - 1;
-      else
-        pv.gq_cjobs[slot] = jp + nj - 1;
-      ++js;
-    }
-    unsigned long long m = rest_mask(i);
-    while (m) {
-      const int h1 = __ffsll(m) - 1;
-      m &= m - 1;
-      int h2 = -1;
-      if (m) {
-        h2 = __ffsll(m) - 1;
-        m &= m - 1;
-      }
-      pv.gq_pairs[jp++] = gq_pair_code(i, h1, h2);
-    }
-  }
-  if (tid == nt - 1) {
-    pv.counts[4] = n_jobs_q;
-    pv.counts[5] = n_full + (n_single + 1) / 2;
-    if (n_single & 1) pv.gq_cjobs2[n_full + n_single / 2] = -1;  // a lone job: rank 1 idles
-  }
-  // pass 5: CTA-pair GEMM-Q jobs: for head pair p, the blocks where both heads
-  // are active, two blocks per job (one per CTA of the pair); then ordered by
-  // first block (counting sort) so the jobs in flight share x tiles in L2
-  if (use_pairs) {
-    __syncthreads();  // scan[] of pass 4 is read
-    const int npair = H >> 1;
+  {
+    const int npair = (H + 1) >> 1;
     int* pcount = scan;  // [npair] jobs per pair, then their offsets
+    auto kind_of = [&](int p, int i) -> int {  // 0: both, 1: first only, 2: second only, -1
+      const int h1 = 2 * p;
+      const unsigned m = (unsigned)(pv.hmask[i] >> h1) & (h1 + 1 < H ? 3u : 1u);
+      return m == 3u ? 0 : m == 1u ? 1 : m == 2u ? 2 : -1;
+    };
     if (tid < npair) {
-      int c = 0;
-#pragma unroll 8
-      for (int i = 0; i < rows; ++i) c += (int)((pv.hmask[i] >> (2 * tid)) & 3ull) == 3;
-      pcount[tid] = (c + 1) >> 1;
+      int n[3] = {0, 0, 0};
+      for (int i = 0; i < rows; ++i) {
+        const int k = kind_of(tid, i);
+        if (k >= 0) ++n[k];
+      }
+      pcount[tid] = (n[0] + 1) / 2 + (n[1] + 1) / 2 + (n[2] + 1) / 2;
     }
     __syncthreads();
     if (tid == 0) {
       int run = 0;
       for (int q = 0; q < npair; ++q) {
-        const int n = pcount[q];
+        const int c = pcount[q];
         pcount[q] = run;
-        run += n;
+        run += c;
       }
       pv.counts[7] = run;
+      pv.counts[4] = 0;
+      pv.counts[5] = 0;
     }
     __syncthreads();
-    int* tmp = pv.gq2_jobs + (H * rows / 2 + 64);  // unsorted jobs
+    int2* tmp = pv.gq_jobs + gq_jobs_cap(H, rows);  // unsorted jobs
     if (tid < npair) {
-      int pos = pcount[tid], pending = -1;
-#pragma unroll 8
+      const int h1 = 2 * tid;
+      int pos = pcount[tid];
+      int pending[3] = {-1, -1, -1};
+      auto emit = [&](int i0, int i1, int k) {
+        const int y = k == 0 ? (h1 | (1 << 8)) : (k == 1 ? h1 : h1 + 1);
+        tmp[pos++] = make_int2(i0 | ((i1 + 1) << 16), y);
+      };
       for (int i = 0; i < rows; ++i) {
-        if ((int)((pv.hmask[i] >> (2 * tid)) & 3ull) != 3) continue;
-        if (pending < 0) {
-          pending = i;
+        const int k = kind_of(tid, i);
+        if (k < 0) continue;
+        if (pending[k] < 0) {
+          pending[k] = i;
         } else {
-          tmp[pos++] = pending | ((i + 1) << 12) | (tid << 24);
-          pending = -1;
+          emit(pending[k], i, k);
+          pending[k] = -1;
         }
       }
-      if (pending >= 0) tmp[pos++] = pending | (tid << 24);
+      for (int k = 0; k < 3; ++k)
+        if (pending[k] >= 0) emit(pending[k], -1, k);
     }
     __syncthreads();
     const int n2 = pv.counts[7];
     int* bcnt = hist;  // [rows] jobs per first block (hist is free after pass 2)
     for (int i = tid; i < rows; i += nt) bcnt[i] = 0;
     __syncthreads();
-    for (int e = tid; e < n2; e += nt) atomicAdd(&bcnt[tmp[e] & 0xFFF], 1);
+    for (int e = tid; e < n2; e += nt) atomicAdd(&bcnt[tmp[e].x & 0xFFFF], 1);
     __syncthreads();
     if (tid == 0) {
       int run = 0;
       for (int i = 0; i < rows; ++i) {
-        const int n = bcnt[i];
+        const int c = bcnt[i];
         bcnt[i] = run;
-        run += n;
+        run += c;
       }
     }
     __syncthreads();
     for (int e = tid; e < n2; e += nt) {
-      const int code = tmp[e];
-      pv.gq2_jobs[atomicAdd(&bcnt[code & 0xFFF], 1)] = code;
+      const int2 code = tmp[e];
+      pv.gq_jobs[atomicAdd(&bcnt[code.x & 0xFFFF], 1)] = code;
     }
-  } else if (tid == 0) {
-    pv.counts[7] = 0;
   }
 }
 

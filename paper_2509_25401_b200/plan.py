@@ -83,8 +83,10 @@ class Plan:
         n = n_waves * ctas
         return self.ws[off:off + 4 * n].view(torch.int32).cpu().numpy().reshape(n_waves, ctas)
 
-    def gq_pairs(self):
-        """GEMM-Q jobs: (block, head1, head2 or -1), one N=256 (or 128) tile each."""
-        n = int(self._view(0, torch.int32, 8)[4].item())
-        it = self._view(6, torch.int32, self.heads * self.rows)[:n].cpu().numpy()
-        return np.stack([it & 0xFFFF, (it >> 16) & 0xFF, (it >> 24) - 1], axis=1)
+    def gq_jobs(self):
+        """GEMM-Q CTA-pair jobs (counts[7]): rows (i0, i1 or -1, h, n256); n256
+        jobs cover heads h and h+1, the others head h alone."""
+        n = int(self.counts()[7])
+        it = self._view(6, torch.int32, 2 * n).view(-1, 2).cpu().numpy()
+        x, y = it[:, 0], it[:, 1]
+        return np.stack([x & 0xFFFF, (x >> 16) - 1, y & 0xFF, (y >> 8) & 1], axis=1)
