@@ -67,6 +67,26 @@ int make_map_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, 
   return FO_OK;
 }
 
+// 3-D bf16 [slabs, rows, cols] map (box box_cols x box_rows x 1): stacked
+// per-order tensors whose row coordinate is clipped / zero-filled per slab
+int make_map3(CUtensorMap* m, const void* base, uint64_t slabs, uint64_t rows, uint64_t cols,
+              uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz, const char* name) {
+  auto fn = encode_fn();
+  if (!fn) return fail(FO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(FO_ERR_PARAM, "%s: base address not 16-byte aligned", name);
+  if ((cols * 2) % 16 != 0) return fail(FO_ERR_SHAPE, "%s: row pitch not a multiple of 16 B", name);
+  cuuint64_t dims[3] = {cols, rows, slabs};
+  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FO_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed (%d)", name, (int)r);
+  return FO_OK;
+}
+
 // box = 64 columns (128 B) x box_rows, SW128: the MMA operand tiles
 // outputs written by row-per-thread 256-bit stores (attention O, GEMM-Q,
 // GEMM-O update out / bias) must start on a 32-byte boundary
@@ -432,12 +452,25 @@ int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int s
                          cm, wm);
   if (rc) return rc;
   if (!cache) return fail(FO_ERR_STATE, "update projection needs the refreshed feature cache");
-  if ((rc = check_align32(out, "out")) || (rc = check_align32(bias, "bias"))) return rc;
+  if (!out || !bias) return fail(FO_ERR_PARAM, "gemm_o_update: out / bias is NULL");
   p.update = 1;
   p.out = static_cast<__nv_bfloat16*>(out);
   p.bias = static_cast<__nv_bfloat16*>(bias);
   p.status = status;
-  launch_gemm_o(am, cm, wm, am, p, num_sms(), (cudaStream_t)stream);
+  // A tiles move in halves (64 rows), each multicast to both CTAs of a cluster;
+  // the cache stacks and the bias are [order+1][S][cols] 3-D maps (a ragged
+  // last block stays inside its order's slab)
+  const uint64_t HD = (uint64_t)heads * kTile;
+  CUtensorMap om, bm;
+  if ((rc = make_map(&am, o, seq, HD, 64, "o"))) return rc;
+  if ((rc = make_map3(&cm, cache, order_d + 1, seq, HD, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B,
+                      "cache")))
+    return rc;
+  if ((rc = make_map_ex(&om, out, seq, d_model, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, "out"))) return rc;
+  if ((rc = make_map3(&bm, bias, order_d + 1, seq, d_model, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B,
+                      "bias")))
+    return rc;
+  launch_gemm_o_update(am, cm, wm, om, bm, p, (cudaStream_t)stream);
   return check_launch("gemm_o_update");
 }
 

@@ -850,24 +850,276 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   }
 }
 
+// =============================================================================
+// GEMM-O update (gemm.py:110-175), 2-CTA clusters like dispatch: both CTAs take
+// the same block i (same K sequences) and neighbouring 256-column n-tiles, and
+// each loads half of every A tile (o or a cache stack) and multicasts it.
+//
+// A d = 0 job (i, n-tile) runs two passes into ONE TMEM accumulator slot:
+//   C pass: the heads cached under the next symbols, A = cache stack 0
+//           -> the slot holds B_c[0]; the epilogue stores it (E1) and hands
+//              the slot back;
+//   A pass: the active heads, A = o, accumulated on top -> the slot holds
+//           B_c[0] + sum_active o W = out; the epilogue stores it (E2).
+// A d >= 1 job (d < orders[i]) is a C pass over cache stack d -> B_c[d].
+// Every head is projected exactly once per order, as in the reference.
+// Two slots (2 x 256 TMEM columns) and jobs taken in pairs (j, j'), issued
+// C(j) C(j') A(j) A(j') on the tensor core while the epilogue runs
+// E1(j) E1(j') E2(j) E2(j'): every epilogue step overlaps the next pass on the
+// other slot, so the tensor core only waits when a store step is longer than
+// a whole pass. The cache and bias are addressed through 3-D maps
+// [order+1][S][cols], so a ragged last block never reads or writes across the
+// slab of the next order.
+// =============================================================================
+namespace gemm {
+constexpr int U_STAGES = 4;
+constexpr int SMEM_BYTES_U = U_STAGES * D_STAGE_BYTES + 2 * OUT_STAGE_BYTES + 1024 + (int)sizeof(Bars);
+static_assert(SMEM_BYTES_U <= 232448, "update shared memory over the sm_100 limit");
+}  // namespace gemm
+
+__global__ void __launch_bounds__(gemm::NTHREADS, 1)
+    gemm_o_update_kernel(const __grid_constant__ CUtensorMap am,  // o [S, H*128], box 64 x 64
+                         const __grid_constant__ CUtensorMap cm,  // cache [D+1][S][H*128], 64 x 64 x 1
+                         const __grid_constant__ CUtensorMap wm,  // W_out^T [dm, H*128], 64 x 128
+                         const __grid_constant__ CUtensorMap om,  // out [S, dm], 32 x 32 SW64
+                         const __grid_constant__ CUtensorMap bm,  // B_c [D+1][S][dm], 32 x 32 x 1 SW64
+                         const GemmOParams p) {
+  using namespace gemm;
+  constexpr int ST = U_STAGES, SB = D_STAGE_BYTES, TBN = D_BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* ostage = smem + ST * SB;
+  Bars* bars = reinterpret_cast<Bars*>(ostage + 2 * OUT_STAGE_BYTES);
+  const int warp = warp_id(), lane = lane_id();
+  const int rank = (int)cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    init_bars(bars, 2, 4);  // a stage is free once both CTAs' MMA warps are done with it
+    tma_prefetch_desc(&am);
+    tma_prefetch_desc(&cm);
+    tma_prefetch_desc(&wm);
+    tma_prefetch_desc(&om);
+    tma_prefetch_desc(&bm);
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+  const int nbn = (p.dm + TBN - 1) / TBN;
+  auto tile_cols = [&](int nb) { return min(TBN, p.dm - nb * TBN); };
+  const int ncb = (nbn + 1) >> 1;  // n-tile pairs per block: one cluster job each
+  const int per_d = p.t_q * ncb;
+  const int n_jobs = (p.order_d + 1) * per_d;
+  const int jstart = (int)(blockIdx.x >> 1), jstep = (int)(gridDim.x >> 1);
+  const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
+  // order-major jobs; d >= 1 jobs exist only for blocks with that many orders
+  // (the same test in both CTAs, so the pair walks identical job lists)
+  auto valid = [&](int w) {
+    const int d = w / per_d;
+    return d == 0 || d < p.orders[(w - d * per_d) / ncb];
+  };
+  auto next_valid = [&](int w) {
+    while (w < n_jobs && !valid(w)) w += jstep;
+    return w;
+  };
+  struct Job {
+    int i, nb, d;
+    bool mine;
+    unsigned long long cached, act;
+  };
+  auto decode = [&](int w) {
+    Job j;
+    j.d = w / per_d;
+    const int rest = w - j.d * per_d;
+    j.i = rest / ncb;
+    j.nb = 2 * (rest - j.i * ncb) + rank;
+    j.mine = j.nb < nbn;
+    j.act = p.hmask[j.i];
+    j.cached = all_heads & ~j.act;
+    return j;
+  };
+  // heads of pass ph (0: C, 1: A) of a job
+  auto pass_mask = [&](const Job& j, int ph) {
+    return ph == 0 ? j.cached : (j.d == 0 ? j.act : 0ull);
+  };
+
+  if (warp == 0) {
+    Ring<ST> rg;
+    for (int w0 = next_valid(jstart); w0 < n_jobs;) {
+      const int w1 = next_valid(w0 + jstep);
+      const int ws[2] = {w0, w1};
+      for (int ph = 0; ph < 2; ++ph)
+        for (int k = 0; k < 2; ++k) {
+          if (ws[k] >= n_jobs) continue;
+          const Job j = decode(ws[k]);
+          unsigned long long m = pass_mask(j, ph);
+          const bool two = j.mine && tile_cols(j.nb) > BN;
+          while (m) {
+            const int h = __ffsll(m) - 1;
+            m &= m - 1;
+            for (int kk = 0; kk < 2; ++kk) {
+              mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+              if (elect_one()) {
+                uint8_t* st = smem + rg.s * SB;
+                mbar_arrive_expect_tx(&bars->full[rg.s],
+                                      A_BYTES + (j.mine ? (two ? 2 : 1) * B_BYTES : 0));
+                if (ph == 0)
+                  tma_load_3d_mc(st + rank * (A_BYTES / 2), &cm, &bars->full[rg.s],
+                                 h * 128 + kk * BK, j.i * BM + rank * (BM / 2), j.d, 0x3);
+                else
+                  tma_load_2d_mc(st + rank * (A_BYTES / 2), &am, &bars->full[rg.s],
+                                 h * 128 + kk * BK, j.i * BM + rank * (BM / 2), 0x3);
+                if (j.mine)
+                  tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, j.nb * TBN);
+                if (two)
+                  tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
+                              j.nb * TBN + BN);
+              }
+              __syncwarp();
+              rg.next();
+            }
+          }
+        }
+      w0 = w1 < n_jobs ? next_valid(w1 + jstep) : n_jobs;
+    }
+    // drain: both CTAs' MMA warps have released every stage
+    for (int k = 0; k < ST; ++k) {
+      mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
+      rg.next();
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc1 = make_idesc_bf16(BM, BN, false, false);
+    const uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, false);
+    const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
+    Ring<ST> rg;
+    int uses[2] = {0, 0};  // passes issued into each slot
+    for (int w0 = next_valid(jstart); w0 < n_jobs;) {
+      const int w1 = next_valid(w0 + jstep);
+      const int ws[2] = {w0, w1};
+      for (int ph = 0; ph < 2; ++ph)
+        for (int k = 0; k < 2; ++k) {
+          if (ws[k] >= n_jobs) continue;
+          const Job j = decode(ws[k]);
+          const uint32_t idesc = (j.mine && tile_cols(j.nb) > BN) ? idesc2 : idesc1;
+          // the slot is free once the epilogue step of its previous pass is done
+          if (uses[k] > 0) {
+            mbar_wait(&bars->tempty[k], (uses[k] - 1) & 1);
+            tc_fence_after();
+          }
+          const int nk = 2 * __popcll(pass_mask(j, ph));
+          // the A pass accumulates onto the C pass's B_c[0]
+          const bool acc0 = ph == 1 && j.cached != 0ull;
+          const uint32_t dslot = tbase + k * D_BN;
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&bars->full[rg.s], rg.ph);
+            tc_fence_after();
+            const uint64_t a = desc0 + (uint64_t)((rg.s * SB) >> 4);
+            if (elect_one()) {
+              if (j.mine) mma_kblock(dslot, a, a + (A_BYTES >> 4), idesc, acc0 || kb > 0);
+              tc_commit_mc(&bars->empty[rg.s], 0x3);
+            }
+            __syncwarp();
+            rg.next();
+          }
+          if (elect_one()) tc_commit(&bars->tfull[k]);
+          __syncwarp();
+          ++uses[k];
+        }
+      w0 = w1 < n_jobs ? next_valid(w1 + jstep) : n_jobs;
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t ostage_u32 = smem_u32(ostage);
+    const int sw = (r >> 1) & 3;  // SW64: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
+    const uint64_t pol = l2_evict_first_policy();
+    int uses[2] = {0, 0};
+    int ob = 0;
+    for (int w0 = next_valid(jstart); w0 < n_jobs;) {
+      const int w1 = next_valid(w0 + jstep);
+      const int ws[2] = {w0, w1};
+      for (int ph = 0; ph < 2; ++ph)
+        for (int k = 0; k < 2; ++k) {
+          if (ws[k] >= n_jobs) continue;
+          const Job j = decode(ws[k]);
+          mbar_wait(&bars->tfull[k], uses[k] & 1);
+          tc_fence_after();
+          ++uses[k];
+          // E1 (after the C pass): B_c[d]; E2 (after the A pass of a d = 0 job): out
+          const bool store = j.mine && (ph == 0 ? (j.cached != 0ull && j.d < p.orders[j.i])
+                                                : j.d == 0);
+          if (!store) {
+            tc_fence_before();
+            mbar_arrive(&bars->tempty[k]);
+            continue;
+          }
+          const int nch = tile_cols(j.nb) / 32;
+          const uint32_t ts = tbase + lane_off + k * D_BN;
+          for (int c = 0; c < nch; ++c) {
+            uint32_t u[32];
+            tmem_ld32(ts + c * 32, u);
+            tmem_ld_wait();
+            if (c == nch - 1) {  // slot drained: the tensor core may take it
+              tc_fence_before();
+              mbar_arrive(&bars->tempty[k]);
+            }
+            uint4 res[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              res[q] = make_uint4(
+                  pack_bf16x2(__uint_as_float(u[8 * q + 0]), __uint_as_float(u[8 * q + 1])),
+                  pack_bf16x2(__uint_as_float(u[8 * q + 2]), __uint_as_float(u[8 * q + 3])),
+                  pack_bf16x2(__uint_as_float(u[8 * q + 4]), __uint_as_float(u[8 * q + 5])),
+                  pack_bf16x2(__uint_as_float(u[8 * q + 6]), __uint_as_float(u[8 * q + 7])));
+            // this warp's 32 rows -> its quarter of staging buffer ob -> one TMA
+            // store; the store that last read the quarter (two chunks ago) is done
+            const uint32_t orow = ostage_u32 + ob * OUT_STAGE_BYTES + r * 64;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sts128(orow + ((q ^ sw) << 4), res[q]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              uint8_t* src = ostage + ob * OUT_STAGE_BYTES + q4 * (OUT_STAGE_BYTES / 4);
+              if (ph == 0)
+                tma_store_3d_hint(&bm, src, j.nb * TBN + c * 32, j.i * BM + q4 * 32, j.d, pol);
+              else
+                tma_store_2d_hint(&om, src, j.nb * TBN + c * 32, j.i * BM + q4 * 32, pol);
+              bulk_commit();
+              bulk_wait_read<1>();
+            }
+            __syncwarp();
+            ob ^= 1;
+          }
+        }
+      w0 = w1 < n_jobs ? next_valid(w1 + jstep) : n_jobs;
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
                    const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_o_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm::SMEM_BYTES);
-    cudaFuncSetAttribute(gemm_o_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm::SMEM_BYTES_D);
-    configured = true;
-  }
-  if (p.update) {
-    note_launch();
-    gemm_o_kernel<true><<<grid, gemm::NTHREADS, gemm::SMEM_BYTES, stream>>>(am, cm, wm, om, p);
-  } else {
-    static int grid_d = 0;
-    launch_pair_clusters(gemm_o_kernel<false>, gemm::SMEM_BYTES_D, &grid_d, stream, am, cm, wm, om,
-                         p);
-  }
+  static int grid_d = 0;
+  launch_pair_clusters(gemm_o_kernel<false>, gemm::SMEM_BYTES_D, &grid_d, stream, am, cm, wm, om, p);
+}
+
+void launch_gemm_o_update(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
+                          const CUtensorMap& om, const CUtensorMap& bm, const GemmOParams& p,
+                          cudaStream_t stream) {
+  static int grid_u = 0;
+  launch_pair_clusters(gemm_o_update_kernel, gemm::SMEM_BYTES_U, &grid_u, stream, am, cm, wm, om, bm,
+                       p);
 }
 
 }  // namespace fo

@@ -213,8 +213,13 @@ struct GemmOParams {
   __nv_bfloat16* bias;                   // [order+1, S, dm]
   uint32_t* status;
 };
+// dispatch (K4): 2-CTA clusters, bias chunks through a TMA ring
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
                    const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream);
+// update (K5): 2-CTA clusters; cm / bm are 3-D [order+1][S][cols] maps
+void launch_gemm_o_update(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
+                          const CUtensorMap& om, const CUtensorMap& bm, const GemmOParams& p,
+                          cudaStream_t stream);
 
 // elementwise helpers
 void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t_q, int order_d,
