@@ -146,6 +146,11 @@ FO_API int fo_synthetic_x(const float* x0, const float* a, const float* b, size_
  * [heads, rows], NULL = all) (attention.py:71-85,128-131). */
 FO_API int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,
                   int rows, int order_d, const uint8_t* select, void* stream);
+/* FeatureCache.update of ONE entry (attention.py:128-131): tile bf16 [r, 128],
+ * r = min(128, seq - 128*block), pushed into (head, block); BOUNDS outside the cache. */
+FO_API int fo_cache_push_tile(const void* tile, void* cache, int32_t* valid, int seq, int heads,
+                              int head_dim, int rows, int order_d, int head, int block,
+                              void* stream);
 
 /* K3 GEMM-Q: q = rope(rms_norm(x @ W_q[h])) for active (block, head) tiles only
  * (gemm.py:44-93, tensor.py:68-109). dense=1: every tile (update phase, plan
@@ -189,6 +194,61 @@ FO_API int fo_generate_masks(const void* q, const void* k, int seq, int heads, i
                              int pool_n, double tau_q, double tau_kv, double s_q, int guard,
                              uint8_t* cache_bits, uint8_t* skip_bits, void* workspace,
                              size_t workspace_bytes, void* stream);
+
+/* ---- The reference's policy building blocks, one stage per call ----------
+ * (policy.py:21-178; fo_generate_masks runs all of them fused.) q, k:
+ * [seq, heads, 128] bf16 (is_f32 = 0) or float32 (is_f32 = 1); a head
+ * dimension head_dim < 128 is zero-padded by the caller (the scores divide by
+ * sqrt(head_dim)). */
+/* compressed_attention (policy.py:44-55): mean-pool q by pool_q and k by
+ * pool_k tokens (tensor.py:112-126), scores / sqrt(d) in float64, row softmax
+ * -> p_tilde float32 [heads, ceil(seq_q/pool_q), ceil(seq_k/pool_k)]. */
+FO_API size_t fo_policy_map_workspace_bytes(int seq_q, int seq_k, int heads, int pool_q,
+                                            int pool_k);
+FO_API int fo_policy_compressed_map(const void* q, const void* k, int is_f32, int seq_q, int seq_k,
+                                    int heads, int head_dim, int pool_q, int pool_k,
+                                    float* p_tilde, void* workspace, size_t workspace_bytes,
+                                    void* stream);
+/* vision_to_text_contribution / text_to_vision_guidance (policy.py:58-77):
+ * float64 contribution [heads, cols - n_t], guidance [heads, rows - n_t]. */
+FO_API int fo_policy_block_scores(const float* p_tilde, int heads, int rows, int cols, int n_t,
+                                  double* contribution, double* guidance, void* stream);
+/* select_cached_blocks (policy.py:93-111): cached u8 [heads, n], 1 = cached. */
+FO_API int fo_policy_select_cached(const double* contribution, const double* guidance, int heads,
+                                   int n, double tau_q, uint8_t* cached, void* stream);
+/* select_skip_blocks (policy.py:124-159): compute u8 [heads, rows] (1 = row
+ * computed) -> keep u8 [heads, rows, cols], 1 = compute the pair. */
+FO_API int fo_policy_select_skip(const float* p_tilde, const uint8_t* compute, int heads, int rows,
+                                 int cols, int n_t, double tau_kv, int guard, uint8_t* keep,
+                                 void* stream);
+
+/* ---- Tile-level building blocks and dense numerics (float32 device buffers) */
+/* online_softmax_update (attention.py:39-49) over one score block: m, l [rows],
+ * acc [rows, d], scores [rows, cols], v [cols, d] -> m_out, l_out, acc_out. */
+FO_API int fo_online_softmax_update(const float* m, const float* l, const float* acc,
+                                    const float* scores, const float* v, int rows, int cols, int d,
+                                    float* m_out, float* l_out, float* acc_out, void* stream);
+/* online_softmax_finalize (attention.py:52-55): out = acc / l; a row with
+ * l <= 0 sets FO_ST_CONSISTENCY. */
+FO_API int fo_online_softmax_finalize(const float* acc, const float* l, int rows, int d, float* out,
+                                      uint32_t* status, void* stream);
+/* update_entry (attention.py:71-85) for one tile of `tile` floats: old_stack
+ * [order+1, tile] with old_valid levels (0 / NULL: no entry) -> stack
+ * [order+1, tile]; valid orders become min(old_valid + 1, order + 1). */
+FO_API int fo_update_entry(const float* old_stack, int old_valid, const float* o_new,
+                           long long tile, int order, float* stack, void* stream);
+/* forecast (attention.py:96-113): out = sum_{d < n_orders} coef[d] * stack[d];
+ * coef is a host array. */
+FO_API int fo_forecast_entry(const float* stack, long long tile, int n_orders, const float* coef,
+                             float* out, void* stream);
+/* tensor.py numerics: mean_pool_blocks (112-126), rms_norm (68-80), rope (83-109;
+ * cos/sin tables float32 [n, d/2]), row_softmax (42-47). x [n, d]. */
+FO_API int fo_mean_pool_blocks(const float* x, int n, int d, int pool, float* out, void* stream);
+FO_API int fo_rms_norm(const float* x, const float* weight, int n, int d, double eps, float* out,
+                       void* stream);
+FO_API int fo_rope(const float* x, const float* cos_t, const float* sin_t, int n, int d, float* out,
+                   void* stream);
+FO_API int fo_row_softmax(const float* s, int n, int d, float* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -246,8 +246,89 @@ def pipeline_run():
     np.savez_compressed(OUT / "run.npz", **d)
 
 
+def api():
+    """The reference's tile-level and policy building blocks on float32 inputs
+    (not bf16-rounded: these device functions compute in float32/float64 like
+    the reference), small d and blocks as the reference's own tests use them
+    (attention.py:21-113, policy.py:21-178, tensor.py:33-126)."""
+    from omniattn import tensor as ref_tensor
+
+    d = {}
+    rng = np.random.default_rng(7)
+    # online softmax over three score blocks, then finalize
+    rows, d_h = 24, 16
+    st = ref_attn.OnlineSoftmaxState.fresh(rows, d_h)
+    for b, cols in enumerate((8, 32, 5)):
+        s_blk = (rng.standard_normal((rows, cols)) * 3).astype(np.float32)
+        v_blk = rng.standard_normal((cols, d_h)).astype(np.float32)
+        d[f"os{b}_scores"], d[f"os{b}_v"] = s_blk, v_blk
+        st = ref_attn.online_softmax_update(st, s_blk, v_blk)
+        d[f"os{b}_m"], d[f"os{b}_l"], d[f"os{b}_acc"] = st.m, st.l, st.acc
+    d["os_final"] = ref_attn.online_softmax_finalize(st)
+    # update_entry / forecast: 4 pushes at order 2 on a ragged tile
+    e = None
+    for t in range(4):
+        o = rng.standard_normal((37, 12)).astype(np.float32)
+        e = ref_attn.update_entry(e, o, 2)
+        d[f"ue{t}_o"], d[f"ue{t}_stack"], d[f"ue{t}_valid"] = o, e.diff_stack, np.array(e.valid_orders)
+        for k, n in ((1, 4), (3, 6)):
+            for od in (0, 1, 2):
+                d[f"ue{t}_fc_{k}_{n}_{od}"] = ref_attn.forecast(e, k, n, od)
+    # tensor.py numerics
+    x = rng.standard_normal((50, 24)).astype(np.float32) * 2
+    w = (1 + 0.1 * rng.standard_normal(24)).astype(np.float32)
+    d["t_x"], d["t_w"] = x, w
+    d["t_rms"] = ref_tensor.rms_norm(x, w)
+    pos = np.arange(50, dtype=np.float64) * 3 + 1
+    d["t_pos"], d["t_rope"] = pos, ref_tensor.rope(x, pos)
+    d["t_rope_vec"] = ref_tensor.rope(x[3], 7.0)
+    d["t_softmax"] = ref_tensor.row_softmax(x)
+    for pool in (1, 4, 7, 64):
+        d[f"t_pool{pool}"] = ref_tensor.mean_pool_blocks(x, pool)
+    a = rng.standard_normal((33, 20)).astype(np.float32)
+    bm = rng.standard_normal((20, 9)).astype(np.float32)
+    d["t_a"], d["t_b"], d["t_matmul"] = a, bm, ref_tensor.matmul(a, bm)
+    q, k, v = (rng.standard_normal((40, 8)).astype(np.float32) for _ in range(3))
+    d["t_q"], d["t_k"], d["t_v"] = q, k, v
+    d["t_dense_attn"] = ref_tensor.dense_attention(q, k, v)
+    # policy building blocks: several geometries, float32 q/k, small d
+    cases = [(96, 8, 8, 8, 16), (100, 16, 4, 4, 9), (130, 4, 10, 5, 0), (256, 32, 8, 8, 40),
+             (77, 12, 7, 7, 14)]
+    for ci, (n, dd, pq_, pk_, n_text) in enumerate(cases):
+        qc = rng.standard_normal((n, dd)).astype(np.float32)
+        kc = (rng.standard_normal((n, dd)) * 1.5).astype(np.float32)
+        m = ref_policy.compressed_attention(qc, kc, pq_, pk_, n_text)
+        d[f"p{ci}_q"], d[f"p{ci}_k"] = qc, kc
+        d[f"p{ci}_cfg"] = np.array([n, dd, pq_, pk_, n_text])
+        d[f"p{ci}_map"], d[f"p{ci}_nt"] = m.p_tilde, np.array(m.n_t)
+        c = ref_policy.vision_to_text_contribution(m)
+        g = ref_policy.text_to_vision_guidance(m)
+        d[f"p{ci}_contrib"], d[f"p{ci}_guid"] = c, g
+        rows, cols = m.p_tilde.shape
+        for ti, tau in enumerate((0.0, 0.3, 0.7, 1.0)):
+            if rows == cols:
+                d[f"p{ci}_cached{ti}"] = ref_policy.select_cached_blocks(c, g, tau)
+            cbits = rng.random(rows) < 0.7
+            d[f"p{ci}_cbits{ti}"] = cbits
+            for guard in (True, False):
+                d[f"p{ci}_keep{ti}_{int(guard)}"] = ref_policy.select_skip_blocks(m, cbits, tau * 0.6, guard=guard)
+            d[f"p{ci}_degrade{ti}"] = ref_policy.degrade_to_full_cache(cbits, m.n_t, 0.25 * ti)
+        if rows == cols and pq_ == pk_:
+            for gi, (tq, tkv, sq, guard) in enumerate(((0.5, 0.3, 0.0, True), (0.8, 0.6, 0.5, False),
+                                                      (0.2, 0.9, 0.1, True))):
+                cb, sb = ref_policy.generate_masks(qc, kc, b_q=pq_, b_k=pk_, pool_n=1, n_text=n_text,
+                                                   tau_q=tq, tau_kv=tkv, s_q=sq, guard=guard)
+                d[f"p{ci}_gm{gi}_cfg"] = np.array([tq, tkv, sq, float(guard)])
+                d[f"p{ci}_gm{gi}_cache"], d[f"p{ci}_gm{gi}_skip"] = cb, sb
+    d["n_policy_cases"] = np.array(len(cases))
+    np.savez_compressed(OUT / "api.npz", **d)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
+    if sys.argv[1:] == ["api"]:
+        api()
+        sys.exit(0)
     if sys.argv[1:] == ["run"]:
         pipeline_run()
         sys.exit(0)
@@ -258,5 +339,6 @@ if __name__ == "__main__":
     gemm_q()
     gemm_o()
     cache_push()
+    api()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

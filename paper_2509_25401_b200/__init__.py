@@ -34,9 +34,14 @@ from .attention import (
     AttnCounters,
     CacheEntry,
     FeatureCache,
+    OnlineSoftmaxState,
     dense_attention_update,
+    forecast,
     forecast_coefficients,
+    online_softmax_finalize,
+    online_softmax_update,
     sparse_attention,
+    update_entry,
 )
 from .gemm import (
     CachedBias,
@@ -77,7 +82,20 @@ from .engine import (
     run,
     synthetic_workload,
 )
-from .policy import MaskPolicy, generate_masks, generate_masks_heads, ramp_threshold
+from .policy import (
+    CompressedAttnMap,
+    MaskPolicy,
+    compressed_attention,
+    degrade_to_full_cache,
+    generate_masks,
+    generate_masks_heads,
+    ramp_threshold,
+    select_cached_blocks,
+    select_skip_blocks,
+    text_to_vision_guidance,
+    vision_to_text_contribution,
+)
+from .tensor import dense_attention, matmul, mean_pool_blocks, rms_norm, rope, row_softmax
 from ._kernels import available_backends, get_backend
 
 __version__ = "0.1.0"

@@ -45,15 +45,30 @@ SIGNATURES = {
     "fo_check_finite": [_P, ctypes.c_longlong, _I, _P, _I, _P, _P],
     "fo_synthetic_x": [_P, _P, _P, _SZ, _I, _F, _F, _F, _P, _P],
     "fo_cache_push": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
+    "fo_cache_push_tile": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P],
     "fo_gemm_q": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _F, _P, _I, _P, _P],
     "fo_gemm_o_update": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "fo_gemm_o_dispatch": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
     "fo_check_active_match": [_P, _P, _I, _I, _I, _P, _P],
     "fo_policy_workspace_bytes": [_I, _I, _I],
     "fo_generate_masks": [_P, _P, _I, _I, _I, _I, _D, _D, _D, _I, _P, _P, _P, _SZ, _P],
+    "fo_policy_map_workspace_bytes": [_I, _I, _I, _I, _I],
+    "fo_policy_compressed_map": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _SZ, _P],
+    "fo_policy_block_scores": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "fo_policy_select_cached": [_P, _P, _I, _I, _D, _P, _P],
+    "fo_policy_select_skip": [_P, _P, _I, _I, _I, _I, _D, _I, _P, _P],
+    "fo_online_softmax_update": [_P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P],
+    "fo_online_softmax_finalize": [_P, _P, _I, _I, _P, _P, _P],
+    "fo_update_entry": [_P, _I, _P, ctypes.c_longlong, _I, _P, _P],
+    "fo_forecast_entry": [_P, ctypes.c_longlong, _I, _P, _P, _P],
+    "fo_mean_pool_blocks": [_P, _I, _I, _I, _P, _P],
+    "fo_rms_norm": [_P, _P, _I, _I, _D, _P, _P],
+    "fo_rope": [_P, _P, _P, _I, _I, _P, _P],
+    "fo_row_softmax": [_P, _I, _I, _P, _P],
 }
 _RESTYPES = {"fo_last_error": ctypes.c_char_p, "fo_plan_workspace_bytes": _SZ,
              "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ,
+             "fo_policy_map_workspace_bytes": _SZ,
              "fo_plan_schedule_offset": _SZ, "fo_kernel_launches": ctypes.c_longlong}
 
 # return codes / status bits (flashomni_b200.h)

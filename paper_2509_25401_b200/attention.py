@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from ._runtime import TILE, Status, check_bsd, check_finite, check_out, require_cuda, stream_ptr
-from .errors import ParameterError, ShapeError, StateError
+from .errors import ConsistencyError, ParameterError, ShapeError, StateError
 from .symbols import DeviceSymbols, SymbolBuffer, ceil_div
 
 DTYPE = np.float32
@@ -110,24 +110,33 @@ class FeatureCache:
         self._sel_keep = sel  # keep alive until the launch retires
 
     def update(self, head, block, o_new):
-        """Reference signature (attention.py:128-131): push one tile. o_new is
-        the tile [rows, 128]; accepted from numpy or torch."""
-        tile = torch.as_tensor(np.asarray(o_new, dtype=np.float32) if not isinstance(o_new, torch.Tensor)
-                               else o_new)
+        """Reference signature (attention.py:128-131): push one tile o_new
+        [rows, 128] (numpy or torch) into entry (head, block). One tile-sized
+        launch on the current stream (fo_cache_push_tile); nothing synchronises
+        for device tiles."""
+        if isinstance(o_new, torch.Tensor):
+            tile = o_new
+            if tile.dim() == 2 and not bool(torch.isfinite(tile).all()):
+                raise ParameterError("tile: contains NaN or Inf")
+        else:
+            arr = np.asarray(o_new, dtype=np.float32)
+            if arr.ndim == 2 and not np.isfinite(arr).all():
+                raise ParameterError("tile: contains NaN or Inf")
+            tile = torch.from_numpy(np.ascontiguousarray(arr))
         if tile.dim() != 2 or tile.shape[1] != TILE:
             raise ShapeError(f"tile shape {tuple(tile.shape)}; head_dim must be {TILE}")
         if self.stacks is None:
             raise ShapeError("allocate the cache with seq= before per-tile updates")
-        r0 = block * TILE
-        rows = min(TILE, self.seq - r0)
+        if not (0 <= head < self.heads and 0 <= block < self.n_blocks):
+            raise IndexError(f"entry ({head}, {block}) outside ({self.heads}, {self.n_blocks})")
+        rows = min(TILE, self.seq - block * TILE)
         if tile.shape[0] != rows:
             raise ShapeError(f"tile shape {tuple(tile.shape)} != cached ({rows}, {TILE})")
-        full = torch.zeros(self.seq, self.heads, TILE, dtype=torch.bfloat16, device=self.device)
-        full[r0:r0 + rows, head] = tile.to(self.device, torch.bfloat16)
-        sel = np.zeros((self.heads, self.n_blocks), np.uint8)
-        sel[head, block] = 1
-        self.push(full, select=sel)
-        torch.cuda.current_stream().synchronize()
+        t = tile.to(self.device, torch.bfloat16).contiguous()
+        _lib.call("fo_cache_push_tile", t.data_ptr(), self.stacks.data_ptr(), self.valid.data_ptr(),
+                  self.seq, self.heads, TILE, self.n_blocks, self.order, int(head), int(block),
+                  stream_ptr(None))
+        self.version += 1
 
     def valid_orders(self, head, block):
         return int(self.valid[head, block].item())
@@ -139,6 +148,122 @@ class FeatureCache:
         rows = min(TILE, self.seq - r0)
         st = self.stacks[:, r0:r0 + rows, head * TILE:(head + 1) * TILE].float().cpu().numpy()
         return CacheEntry(diff_stack=st, valid_orders=self.valid_orders(head, block))
+
+
+# ---------------------------------------------------------------------------
+# Tile-level building blocks of the reference API (attention.py:21-113), on
+# the device (csrc/fo_numerics.cu). numpy in -> numpy out, torch in -> torch.
+
+
+def _f32(a, name=None, finite=False):
+    host = not isinstance(a, torch.Tensor)
+    require_cuda()
+    t = torch.as_tensor(np.asarray(a, dtype=DTYPE)) if host else a
+    t = t.to("cuda" if host or not t.is_cuda else t.device, torch.float32).contiguous()
+    if finite and not bool(torch.isfinite(t).all()):
+        raise ParameterError(f"{name}: contains NaN or Inf")
+    return t, host
+
+
+def _back(t, host):
+    return t.cpu().numpy() if host else t
+
+
+@dataclass
+class OnlineSoftmaxState:
+    """Running max, normalizer and unnormalized accumulator per query row
+    (attention.py:21-36)."""
+
+    m: object
+    l: object
+    acc: object
+
+    @classmethod
+    def fresh(cls, rows, d):
+        return cls(m=np.full(rows, -np.inf, dtype=DTYPE), l=np.zeros(rows, dtype=DTYPE),
+                   acc=np.zeros((rows, d), dtype=DTYPE))
+
+
+def online_softmax_update(state, scores, v_block):
+    """Fold one score block into the running softmax state (attention.py:39-49),
+    one CTA per row (fo_online_softmax_update)."""
+    s, host = _f32(scores)
+    v, _ = _f32(v_block)
+    m, _ = _f32(state.m)
+    l, _ = _f32(state.l)
+    acc, _ = _f32(state.acc)
+    if s.dim() != 2 or v.dim() != 2 or acc.dim() != 2:
+        raise ShapeError("online_softmax_update: scores, v_block and acc must be 2-D")
+    rows, cols = s.shape
+    d = v.shape[1]
+    if v.shape[0] != cols or tuple(acc.shape) != (rows, d) or m.numel() != rows or l.numel() != rows:
+        raise ShapeError(f"online_softmax_update: scores {tuple(s.shape)}, v {tuple(v.shape)}, "
+                         f"acc {tuple(acc.shape)}, m/l {m.numel()}/{l.numel()}")
+    m_o, l_o, acc_o = torch.empty_like(m), torch.empty_like(l), torch.empty_like(acc)
+    _lib.call("fo_online_softmax_update", m.data_ptr(), l.data_ptr(), acc.data_ptr(), s.data_ptr(),
+              v.data_ptr(), rows, cols, d, m_o.data_ptr(), l_o.data_ptr(), acc_o.data_ptr(),
+              stream_ptr(None))
+    return OnlineSoftmaxState(m=_back(m_o, host), l=_back(l_o, host), acc=_back(acc_o, host))
+
+
+def online_softmax_finalize(state):
+    """Normalize the accumulator, diag(l)^-1 acc (attention.py:52-55); an empty
+    row (l <= 0) raises ConsistencyError."""
+    acc, host = _f32(state.acc)
+    l, _ = _f32(state.l)
+    if acc.dim() != 2 or l.numel() != acc.shape[0]:
+        raise ShapeError("online_softmax_finalize: acc must be [rows, d] with one l per row")
+    out = torch.empty_like(acc)
+    st = Status.default()
+    st.check("online_softmax_finalize")
+    _lib.call("fo_online_softmax_finalize", acc.data_ptr(), l.data_ptr(), acc.shape[0],
+              acc.shape[1], out.data_ptr(), st.ptr(), stream_ptr(None))
+    bits = int(st.t.item())
+    if bits:
+        st.t.zero_()
+        raise ConsistencyError("softmax state finalized with an empty row")
+    return _back(out, host)
+
+
+def update_entry(entry, o_new, order):
+    """Push a fresh tile output, shifting differences one level deeper
+    (attention.py:71-85): stack[0] = o_new, stack[d] = stack[d-1] - old[d-1]
+    for d < valid = min(old valid + 1, order + 1) (fo_update_entry)."""
+    o, host = _f32(o_new, "tile", finite=True)
+    if o.dim() != 2:
+        raise ShapeError(f"tile: expected a 2-D matrix, got shape {tuple(o.shape)}")
+    if order < 0:
+        raise ParameterError(f"order must be >= 0, got {order}")
+    stack = torch.empty((order + 1,) + tuple(o.shape), dtype=torch.float32, device=o.device)
+    old, old_valid = None, 0
+    if entry is not None:
+        old, _ = _f32(entry.diff_stack)
+        if tuple(old.shape[1:]) != tuple(o.shape):
+            raise ShapeError(f"tile shape {tuple(o.shape)} != cached {tuple(old.shape[1:])}")
+        old_valid = min(int(entry.valid_orders), old.shape[0])
+    _lib.call("fo_update_entry", None if old is None else old.data_ptr(), old_valid, o.data_ptr(),
+              o.numel(), int(order), stack.data_ptr(), stream_ptr(None))
+    valid = 1 if entry is None else min(int(entry.valid_orders) + 1, order + 1)
+    return CacheEntry(diff_stack=_back(stack, host), valid_orders=valid)
+
+
+def forecast(entry, elapsed_k, interval_n, order_d):
+    """Extrapolate a cached tile elapsed_k steps past its last update
+    (attention.py:96-113): sum_{d < min(order_d+1, valid)} c_d * stack[d]
+    (fo_forecast_entry). StateError for a cold entry, then ParameterError for
+    elapsed_k outside [1, N-1], in the reference's order."""
+    if entry is None or entry.valid_orders < 1:
+        raise StateError("forecast requested from a cold cache entry")
+    check_elapsed(elapsed_k, interval_n)
+    st, host = _f32(entry.diff_stack)
+    n_orders = min(order_d + 1, int(entry.valid_orders))
+    coef = forecast_coefficients(elapsed_k, interval_n, n_orders)
+    c = (ctypes.c_float * len(coef))(*coef.tolist())
+    tile = st[0].numel()
+    out = torch.empty(tuple(st.shape[1:]), dtype=torch.float32, device=st.device)
+    _lib.call("fo_forecast_entry", st.data_ptr(), tile, n_orders, ctypes.addressof(c),
+              out.data_ptr(), stream_ptr(None))
+    return _back(out, host)
 
 
 # ---------------------------------------------------------------------------

@@ -16,7 +16,7 @@ import sys
 
 HERE = pathlib.Path(__file__).resolve().parent
 SOURCES = ["fo_symbols.cu", "fo_attention.cu", "fo_attention_cs.cu", "fo_gemm.cu",
-           "fo_elementwise.cu", "fo_policy.cu", "fo_capi.cu"]
+           "fo_elementwise.cu", "fo_policy.cu", "fo_numerics.cu", "fo_capi.cu"]
 OUT = HERE / "_fo_b200.so"
 OBJ_DIR = HERE / "build"
 NVCC_FLAGS = [

@@ -372,8 +372,25 @@ int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads
   if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
   if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
   launch_cache_push(static_cast<const __nv_bfloat16*>(o), static_cast<__nv_bfloat16*>(cache), valid,
-                    seq, heads, rows, order_d, select, (cudaStream_t)stream);
+                    seq, heads, rows, order_d, select, -1, (cudaStream_t)stream);
   return check_launch("cache_push");
+}
+
+int fo_cache_push_tile(const void* tile, void* cache, int32_t* valid, int seq, int heads,
+                       int head_dim, int rows, int order_d, int head, int block, void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (!tile || !cache || !valid) return fail(FO_ERR_PARAM, "cache_push_tile: null pointer");
+  if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
+  if (order_d < 0 || order_d > 3) return fail(FO_ERR_PARAM, "order_d must be in [0, 3]");
+  if (head < 0 || head >= heads || block < 0 || block >= rows)
+    return fail(FO_ERR_BOUNDS, "cache_push_tile: entry (%d, %d) outside (%d, %d)", head, block,
+                heads, rows);
+  if (reinterpret_cast<uintptr_t>(tile) & 15) return fail(FO_ERR_PARAM, "cache_push_tile: tile misaligned");
+  launch_cache_push(static_cast<const __nv_bfloat16*>(tile), static_cast<__nv_bfloat16*>(cache),
+                    valid, seq, heads, rows, order_d, nullptr, head * rows + block,
+                    (cudaStream_t)stream);
+  return check_launch("cache_push_tile");
 }
 
 int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, int head_dim,
@@ -552,6 +569,156 @@ int fo_generate_masks(const void* q, const void* k, int seq, int heads, int n_te
       pool_n, tau_q, tau_kv, s_q, guard, cache_bits, skip_bits, workspace, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(FO_ERR_CUDA, "generate_masks: %s", cudaGetErrorString(e));
   return FO_OK;
+}
+
+// ---- the reference's policy building blocks, one stage per call (policy.py:21-178)
+size_t fo_policy_map_workspace_bytes(int seq_q, int seq_k, int heads, int pool_q, int pool_k) {
+  if (seq_q <= 0 || seq_k <= 0 || heads <= 0 || pool_q <= 0 || pool_k <= 0) return 0;
+  return policy_map_workspace_bytes(heads, (seq_q + pool_q - 1) / pool_q,
+                                    (seq_k + pool_k - 1) / pool_k);
+}
+
+int fo_policy_compressed_map(const void* q, const void* k, int is_f32, int seq_q, int seq_k,
+                             int heads, int head_dim, int pool_q, int pool_k, float* p_tilde,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  if (!q || !k || !p_tilde || !workspace) return fail(FO_ERR_PARAM, "compressed_map: null pointer");
+  if (seq_q <= 0 || seq_k <= 0 || heads <= 0)
+    return fail(FO_ERR_SHAPE, "compressed_map: seq=%d/%d heads=%d", seq_q, seq_k, heads);
+  if (head_dim < 1 || head_dim > kTile)
+    return fail(FO_ERR_SHAPE, "compressed_map: head_dim %d outside [1, %d]", head_dim, kTile);
+  if (pool_q < 1 || pool_k < 1)  // mean_pool_blocks (tensor.py:119-120)
+    return fail(FO_ERR_PARAM, "pool must be >= 1, got %d / %d", pool_q, pool_k);
+  const int rows = (seq_q + pool_q - 1) / pool_q, cols = (seq_k + pool_k - 1) / pool_k;
+  if (rows > kPolicyMaxBlocks || cols > kPolicyMaxBlocks)
+    return fail(FO_ERR_SHAPE, "compressed_map: %d x %d compressed blocks exceed %d", rows, cols,
+                kPolicyMaxBlocks);
+  if (workspace_bytes < policy_map_workspace_bytes(heads, rows, cols))
+    return fail(FO_ERR_PARAM, "compressed_map: workspace %zu B too small", workspace_bytes);
+  const uintptr_t al = is_f32 ? 8 : 4;
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) % al)
+    return fail(FO_ERR_PARAM, "compressed_map: q/k misaligned");
+  cudaError_t e = launch_policy_map(q, k, is_f32, seq_q, seq_k, heads, head_dim, pool_q, pool_k,
+                                    p_tilde, workspace, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "compressed_map: %s", cudaGetErrorString(e));
+  return FO_OK;
+}
+
+int fo_policy_block_scores(const float* p_tilde, int heads, int rows, int cols, int n_t,
+                           double* contribution, double* guidance, void* stream) {
+  if (!p_tilde || !contribution || !guidance) return fail(FO_ERR_PARAM, "block_scores: null pointer");
+  if (heads <= 0 || rows <= 0 || cols <= 0 || rows > kPolicyMaxBlocks || cols > kPolicyMaxBlocks)
+    return fail(FO_ERR_SHAPE, "block_scores: %d x %d map", rows, cols);
+  if (n_t < 0 || n_t >= rows || n_t > cols)  // CompressedAttnMap (policy.py:33-37)
+    return fail(FO_ERR_PARAM, "n_t=%d must leave at least one vision row (map has %d rows)", n_t, rows);
+  cudaError_t e = launch_policy_scores(p_tilde, heads, rows, cols, n_t, contribution, guidance,
+                                       (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "block_scores: %s", cudaGetErrorString(e));
+  return FO_OK;
+}
+
+int fo_policy_select_cached(const double* contribution, const double* guidance, int heads, int n,
+                            double tau_q, uint8_t* cached, void* stream) {
+  if (!contribution || !guidance || !cached) return fail(FO_ERR_PARAM, "select_cached: null pointer");
+  if (heads <= 0 || n < 0 || n > kPolicyMaxBlocks) return fail(FO_ERR_SHAPE, "select_cached: n=%d", n);
+  if (!(tau_q >= 0.0 && tau_q <= 1.0)) return fail(FO_ERR_PARAM, "tau_q must be in [0, 1], got %g", tau_q);
+  if (n == 0) return FO_OK;
+  cudaError_t e = launch_policy_select_cached(contribution, guidance, heads, n, tau_q, cached,
+                                              (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "select_cached: %s", cudaGetErrorString(e));
+  return FO_OK;
+}
+
+int fo_policy_select_skip(const float* p_tilde, const uint8_t* compute, int heads, int rows,
+                          int cols, int n_t, double tau_kv, int guard, uint8_t* keep, void* stream) {
+  if (!p_tilde || !compute || !keep) return fail(FO_ERR_PARAM, "select_skip: null pointer");
+  if (heads <= 0 || rows <= 0 || cols <= 0 || rows > kPolicyMaxBlocks || cols > kPolicyMaxBlocks)
+    return fail(FO_ERR_SHAPE, "select_skip: %d x %d map", rows, cols);
+  if (n_t < 0 || n_t > cols) return fail(FO_ERR_PARAM, "select_skip: n_t=%d", n_t);
+  if (!(tau_kv >= 0.0 && tau_kv <= 1.0))
+    return fail(FO_ERR_PARAM, "tau_kv must be in [0, 1], got %g", tau_kv);
+  cudaError_t e = launch_policy_select_skip(p_tilde, compute, heads, rows, cols, n_t, tau_kv, guard,
+                                            keep, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(FO_ERR_CUDA, "select_skip: %s", cudaGetErrorString(e));
+  return FO_OK;
+}
+
+// ---- tile-level building blocks and dense numerics (fo_numerics.cu)
+static int cuda_rc(cudaError_t e, const char* what) {
+  return e == cudaSuccess ? FO_OK : fail(FO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int fo_online_softmax_update(const float* m, const float* l, const float* acc, const float* scores,
+                             const float* v, int rows, int cols, int d, float* m_out, float* l_out,
+                             float* acc_out, void* stream) {
+  if (!m || !l || !acc || !scores || !v || !m_out || !l_out || !acc_out)
+    return fail(FO_ERR_PARAM, "online_softmax_update: null pointer");
+  if (rows < 0 || cols <= 0 || d <= 0 || cols > max_row_width())
+    return fail(FO_ERR_SHAPE, "online_softmax_update: rows=%d cols=%d d=%d", rows, cols, d);
+  if (rows == 0) return FO_OK;
+  return cuda_rc(launch_online_softmax_update(m, l, acc, scores, v, rows, cols, d, m_out, l_out,
+                                              acc_out, (cudaStream_t)stream),
+                 "online_softmax_update");
+}
+
+int fo_online_softmax_finalize(const float* acc, const float* l, int rows, int d, float* out,
+                               uint32_t* status, void* stream) {
+  if (!acc || !l || !out || !status) return fail(FO_ERR_PARAM, "online_softmax_finalize: null pointer");
+  if (rows < 0 || d <= 0) return fail(FO_ERR_SHAPE, "online_softmax_finalize: rows=%d d=%d", rows, d);
+  if (rows == 0) return FO_OK;
+  return cuda_rc(launch_online_softmax_finalize(acc, l, rows, d, out, status, (cudaStream_t)stream),
+                 "online_softmax_finalize");
+}
+
+int fo_update_entry(const float* old_stack, int old_valid, const float* o_new, long long tile,
+                    int order, float* stack, void* stream) {
+  if (!o_new || !stack || (old_valid > 0 && !old_stack))
+    return fail(FO_ERR_PARAM, "update_entry: null pointer");
+  if (order < 0 || order > 7 || tile < 0) return fail(FO_ERR_PARAM, "update_entry: order %d", order);
+  if (tile == 0) return FO_OK;
+  const int valid = old_valid > 0 ? (old_valid + 1 < order + 1 ? old_valid + 1 : order + 1) : 1;
+  return cuda_rc(launch_update_entry(old_stack, o_new, (size_t)tile, order, valid, stack,
+                                     (cudaStream_t)stream),
+                 "update_entry");
+}
+
+int fo_forecast_entry(const float* stack, long long tile, int n_orders, const float* coef,
+                      float* out, void* stream) {
+  if (!stack || !coef || !out) return fail(FO_ERR_PARAM, "forecast: null pointer");
+  if (n_orders < 1 || n_orders > 8 || tile < 0) return fail(FO_ERR_PARAM, "forecast: n_orders %d", n_orders);
+  if (tile == 0) return FO_OK;
+  return cuda_rc(launch_forecast_entry(stack, (size_t)tile, n_orders, coef, out, (cudaStream_t)stream),
+                 "forecast");
+}
+
+int fo_mean_pool_blocks(const float* x, int n, int d, int pool, float* out, void* stream) {
+  if (!x || !out) return fail(FO_ERR_PARAM, "mean_pool_blocks: null pointer");
+  if (pool < 1) return fail(FO_ERR_PARAM, "pool must be >= 1, got %d", pool);
+  if (n < 0 || d <= 0) return fail(FO_ERR_SHAPE, "mean_pool_blocks: n=%d d=%d", n, d);
+  if (n == 0) return FO_OK;
+  return cuda_rc(launch_mean_pool(x, n, d, pool, out, (cudaStream_t)stream), "mean_pool_blocks");
+}
+
+int fo_rms_norm(const float* x, const float* weight, int n, int d, double eps, float* out,
+                void* stream) {
+  if (!x || !weight || !out) return fail(FO_ERR_PARAM, "rms_norm: null pointer");
+  if (n < 0 || d <= 0 || d > max_row_width()) return fail(FO_ERR_SHAPE, "rms_norm: n=%d d=%d", n, d);
+  if (n == 0) return FO_OK;
+  return cuda_rc(launch_rms_norm(x, weight, n, d, eps, out, (cudaStream_t)stream), "rms_norm");
+}
+
+int fo_rope(const float* x, const float* cos_t, const float* sin_t, int n, int d, float* out,
+            void* stream) {
+  if (!x || !cos_t || !sin_t || !out) return fail(FO_ERR_PARAM, "rope: null pointer");
+  if (n < 0 || d <= 0 || d % 2) return fail(FO_ERR_SHAPE, "rope: feature dim must be even, got %d", d);
+  if (n == 0) return FO_OK;
+  return cuda_rc(launch_rope(x, cos_t, sin_t, n, d, out, (cudaStream_t)stream), "rope");
+}
+
+int fo_row_softmax(const float* s, int n, int d, float* out, void* stream) {
+  if (!s || !out) return fail(FO_ERR_PARAM, "row_softmax: null pointer");
+  if (n < 0 || d <= 0 || d > max_row_width()) return fail(FO_ERR_SHAPE, "row_softmax: n=%d d=%d", n, d);
+  if (n == 0) return FO_OK;
+  return cuda_rc(launch_row_softmax(s, n, d, out, (cudaStream_t)stream), "row_softmax");
 }
 
 }  // extern "C"

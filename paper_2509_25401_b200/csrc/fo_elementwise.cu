@@ -48,8 +48,10 @@ __global__ void forecast_materialize_kernel(const __nv_bfloat16* __restrict__ ca
 
 __global__ void cache_push_kernel(const __nv_bfloat16* __restrict__ o, __nv_bfloat16* __restrict__ cache,
                                   int32_t* __restrict__ valid, int S, int H, int t_q, int order_d,
-                                  const uint8_t* __restrict__ sel) {
-  const int tile = blockIdx.x;
+                                  const uint8_t* __restrict__ sel, int one_tile) {
+  // one_tile >= 0: a single (head, block) entry h * t_q + i whose fresh output
+  // `o` is that tile alone, [rows, 128] (FeatureCache.update, attention.py:128-131)
+  const int tile = one_tile >= 0 ? one_tile : blockIdx.x;
   const int h = tile / t_q, i = tile % t_q;
   if (sel && !sel[(size_t)h * t_q + i]) return;
   const int valid_old = valid[(size_t)h * t_q + i];
@@ -60,7 +62,8 @@ __global__ void cache_push_kernel(const __nv_bfloat16* __restrict__ o, __nv_bflo
   for (int e = threadIdx.x; e < rows * 16; e += blockDim.x) {
     const int rr = e >> 4, v = e & 15;
     const size_t off = (size_t)(i * kTile + rr) * HD + (size_t)h * kTile + v * 8;
-    const uint4 ov = *reinterpret_cast<const uint4*>(o + off);
+    const size_t o_off = one_tile >= 0 ? (size_t)rr * kTile + v * 8 : off;
+    const uint4 ov = *reinterpret_cast<const uint4*>(o + o_off);
     float cur[8] = {bf16lo(ov.x), bf16hi(ov.x), bf16lo(ov.y), bf16hi(ov.y),
                     bf16lo(ov.z), bf16hi(ov.z), bf16lo(ov.w), bf16hi(ov.w)};
     for (int d = 0; d <= order_d; ++d) {
@@ -166,9 +169,10 @@ void launch_forecast_materialize(const __nv_bfloat16* cache, int S, int H, int t
 }
 
 void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,
-                       int t_q, int order_d, const uint8_t* sel, cudaStream_t stream) {
+                       int t_q, int order_d, const uint8_t* sel, int one_tile, cudaStream_t stream) {
   note_launch();
-  cache_push_kernel<<<H * t_q, 256, 0, stream>>>(o, cache, valid, S, H, t_q, order_d, sel);
+  cache_push_kernel<<<one_tile >= 0 ? 1 : H * t_q, 256, 0, stream>>>(o, cache, valid, S, H, t_q,
+                                                                     order_d, sel, one_tile);
 }
 
 }  // namespace fo

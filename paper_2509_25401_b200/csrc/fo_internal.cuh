@@ -230,7 +230,8 @@ void launch_check_finite(const void* data, long long rows, int cols,
 void launch_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind,
                         float c1, float c2, float s, __nv_bfloat16* out, cudaStream_t stream);
 void launch_cache_push(const __nv_bfloat16* o, __nv_bfloat16* cache, int32_t* valid, int S, int H,
-                       int t_q, int order_d, const uint8_t* sel, cudaStream_t stream);
+                       int t_q, int order_d, const uint8_t* sel, int one_tile,
+                       cudaStream_t stream);
 
 // update-step mask policy (fo_policy.cu)
 constexpr int kPolicyMaxBlocks = 1024;  // compressed blocks per side
@@ -239,5 +240,36 @@ cudaError_t launch_generate_masks(const __nv_bfloat16* q, const __nv_bfloat16* k
                                   int n_t, int pool_n, double tau_q, double tau_kv, double s_q,
                                   int guard, uint8_t* cache_bits, uint8_t* skip_bits, void* ws,
                                   cudaStream_t stream);
+// the reference's policy building blocks one stage at a time (policy.py:21-178)
+size_t policy_map_workspace_bytes(int H, int rows_q, int rows_k);
+cudaError_t launch_policy_map(const void* q, const void* k, int is_f32, int S_q, int S_k, int H,
+                              int d, int pool_q, int pool_k, float* p_tilde, void* ws,
+                              cudaStream_t stream);
+cudaError_t launch_policy_scores(const float* p_tilde, int H, int rows, int cols, int n_t,
+                                 double* contribution, double* guidance, cudaStream_t stream);
+cudaError_t launch_policy_select_cached(const double* contribution, const double* guidance, int H,
+                                        int V, double tau_q, uint8_t* cached, cudaStream_t stream);
+cudaError_t launch_policy_select_skip(const float* p_tilde, const uint8_t* compute, int H, int rows,
+                                      int cols, int n_t, double tau_kv, int guard, uint8_t* keep,
+                                      cudaStream_t stream);
+
+// tile-level building blocks and dense numerics (fo_numerics.cu)
+int max_row_width();
+cudaError_t launch_online_softmax_update(const float* m, const float* l, const float* acc,
+                                         const float* scores, const float* v, int rows, int cols,
+                                         int d, float* m_out, float* l_out, float* acc_out,
+                                         cudaStream_t st);
+cudaError_t launch_online_softmax_finalize(const float* acc, const float* l, int rows, int d,
+                                           float* out, uint32_t* status, cudaStream_t st);
+cudaError_t launch_update_entry(const float* old, const float* o, size_t tile, int order, int valid,
+                                float* stack, cudaStream_t st);
+cudaError_t launch_forecast_entry(const float* stack, size_t tile, int n_orders, const float* coef,
+                                  float* out, cudaStream_t st);
+cudaError_t launch_mean_pool(const float* x, int n, int d, int pool, float* out, cudaStream_t st);
+cudaError_t launch_rms_norm(const float* x, const float* w, int n, int d, double eps, float* out,
+                            cudaStream_t st);
+cudaError_t launch_rope(const float* x, const float* cs, const float* sn, int n, int d, float* out,
+                        cudaStream_t st);
+cudaError_t launch_row_softmax(const float* s, int n, int d, float* out, cudaStream_t st);
 
 }  // namespace fo

@@ -1,0 +1,266 @@
+// The reference's tile-level building blocks on the device: the online-softmax
+// recurrence (attention.py:21-55), one cache entry's update / forecast
+// (attention.py:71-113) and the dense numerics of tensor.py:33-126 that the
+// policy and the tests build on. These are the operator API's small pieces,
+// not the layer hot path (that is the batched kernels of fo_attention_cs.cu,
+// fo_gemm.cu, fo_policy.cu); they follow numpy's float32 / float64 arithmetic
+// so results match the reference bit for bit where numpy's order is fixed
+// (sequential / pairwise sums, single-rounded products: __fmul_rn / __fadd_rn
+// keep nvcc from contracting into FMAs), and within float32 rounding where it
+// is BLAS- or libm-defined (p @ v, exp).
+#include "fo_internal.cuh"
+#include "fo_numpy.cuh"
+
+namespace fo {
+
+namespace {
+
+constexpr int kRowThreads = 128;
+
+__device__ float block_max(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float m = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
+  return m;
+}
+
+// numpy maximum: NaN propagates
+__device__ __forceinline__ float np_maximum(float a, float b) {
+  return (a != a || b != b) ? __int_as_float(0x7fc00000) : fmaxf(a, b);
+}
+
+// CTA per query row (attention.py:39-49):
+//   m' = max(m, rowmax(S)); corr = exp(m - m'); p = exp(S - m')
+//   l' = l*corr + sum(p); acc' = acc*corr + p @ V
+__global__ void __launch_bounds__(kRowThreads)
+online_softmax_update_kernel(const float* __restrict__ m, const float* __restrict__ l,
+                             const float* __restrict__ acc, const float* __restrict__ scores,
+                             const float* __restrict__ v, int cols, int d, float* __restrict__ m_out,
+                             float* __restrict__ l_out, float* __restrict__ acc_out) {
+  extern __shared__ float p_s[];  // [cols]
+  __shared__ float red[kRowThreads / 32];
+  __shared__ float s_corr, s_m;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const float* srow = scores + (size_t)r * cols;
+  float mx = -INFINITY;
+  bool nan = false;
+  for (int c = tid; c < cols; c += blockDim.x) {
+    const float x = srow[c];
+    nan |= x != x;
+    mx = fmaxf(mx, x);
+  }
+  mx = block_max(mx, red);
+  nan = __syncthreads_or(nan);
+  if (tid == 0) {
+    const float m_new = np_maximum(m[r], nan ? __int_as_float(0x7fc00000) : mx);
+    s_m = m_new;
+    s_corr = expf(__fsub_rn(m[r], m_new));
+  }
+  __syncthreads();
+  const float m_new = s_m, corr = s_corr;
+  for (int c = tid; c < cols; c += blockDim.x) p_s[c] = expf(__fsub_rn(srow[c], m_new));
+  __syncthreads();
+  if (tid == 0) {
+    m_out[r] = m_new;
+    l_out[r] = __fadd_rn(__fmul_rn(l[r], corr), pairwise_sum<8, float>(p_s, cols));
+  }
+  for (int j = tid; j < d; j += blockDim.x) {
+    float pv = 0.f;
+    for (int c = 0; c < cols; ++c) pv = fmaf(p_s[c], v[(size_t)c * d + j], pv);
+    acc_out[(size_t)r * d + j] = __fadd_rn(__fmul_rn(acc[(size_t)r * d + j], corr), pv);
+  }
+}
+
+// diag(l)^-1 acc (attention.py:52-55); an empty row (l <= 0) is a
+// ConsistencyError, latched in the status word
+__global__ void online_softmax_finalize_kernel(const float* __restrict__ acc,
+                                               const float* __restrict__ l, int rows, int d,
+                                               float* __restrict__ out, uint32_t* status) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)rows * d) return;
+  const float li = l[i / d];
+  if (li <= 0.f && i % d == 0) raise_status(status, ST_CONSISTENCY);
+  out[i] = __fdiv_rn(acc[i], li);
+}
+
+// update_entry (attention.py:71-85): stack[0] = o; stack[k] = stack[k-1] - old[k-1]
+// for k < valid; deeper levels zero. One thread per tile element.
+__global__ void update_entry_kernel(const float* __restrict__ old, const float* __restrict__ o,
+                                    size_t tile, int order, int valid, float* __restrict__ stack) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tile) return;
+  float prev = o[i];
+  stack[i] = prev;
+  for (int k = 1; k <= order; ++k) {
+    prev = k < valid ? __fsub_rn(prev, old[(size_t)(k - 1) * tile + i]) : 0.f;
+    stack[(size_t)k * tile + i] = prev;
+  }
+}
+
+struct Coef {
+  float c[8];
+};
+
+// forecast (attention.py:96-113): out = c0*stack[0]; out += c_d*stack[d]
+__global__ void forecast_entry_kernel(const float* __restrict__ stack, size_t tile, int n_orders,
+                                      Coef coef, float* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tile) return;
+  float acc = __fmul_rn(coef.c[0], stack[i]);
+  for (int k = 1; k < n_orders; ++k)
+    acc = __fadd_rn(acc, __fmul_rn(coef.c[k], stack[(size_t)k * tile + i]));
+  out[i] = acc;
+}
+
+// mean_pool_blocks (tensor.py:112-126): np.add.reduceat in float64 from the
+// block's first row, / actual length, -> float32. Thread per (block, column).
+__global__ void mean_pool_kernel(const float* __restrict__ x, int n, int d, int pool, int blocks,
+                                 float* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)blocks * d) return;
+  const int c = (int)(i % d), b = (int)(i / d);
+  const int s0 = b * pool, s1 = min(n, s0 + pool);
+  double a = 0.0;
+  for (int s = s0; s < s1; ++s) a += (double)x[(size_t)s * d + c];
+  out[i] = (float)(a / (double)(s1 - s0));
+}
+
+// rms_norm (tensor.py:68-80): ms = pairwise fp64 mean of x^2; y = fp32(x*w) * (1/sqrt(ms+eps))
+// in fp64, -> fp32. CTA per row.
+__global__ void __launch_bounds__(kRowThreads)
+rms_norm_kernel(const float* __restrict__ x, const float* __restrict__ w, int d, double eps,
+                float* __restrict__ out) {
+  extern __shared__ double sq[];  // [d]
+  __shared__ double s_inv;
+  const float* xr = x + (size_t)blockIdx.x * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const double v = (double)xr[c];
+    sq[c] = v * v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double ms = pairwise_sum<10, double>(sq, d) / (double)d;
+    s_inv = 1.0 / sqrt(ms + eps);
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    out[(size_t)blockIdx.x * d + c] = (float)((double)__fmul_rn(xr[c], w[c]) * inv);
+}
+
+// rope (tensor.py:83-109), interleaved pairs, cos/sin tables fp32 [n, d/2]
+// (float64 angles cast once, as the reference computes them)
+__global__ void rope_kernel(const float* __restrict__ x, const float* __restrict__ cs,
+                            const float* __restrict__ sn, int n, int d, float* __restrict__ out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int half = d / 2;
+  if (i >= (size_t)n * half) return;
+  const size_t r = i / half;
+  const int j = (int)(i % half);
+  const float e = x[r * d + 2 * j], o = x[r * d + 2 * j + 1];
+  const float c = cs[i], s = sn[i];
+  out[r * d + 2 * j] = __fsub_rn(__fmul_rn(e, c), __fmul_rn(o, s));
+  out[r * d + 2 * j + 1] = __fadd_rn(__fmul_rn(e, s), __fmul_rn(o, c));
+}
+
+// row_softmax (tensor.py:42-47): fp64 exp(s - rowmax), pairwise fp64 row sum,
+// e / sum -> fp32. CTA per row.
+__global__ void __launch_bounds__(kRowThreads)
+row_softmax_kernel(const float* __restrict__ s, int d, float* __restrict__ out) {
+  extern __shared__ double e_s[];  // [d]
+  __shared__ float red[kRowThreads / 32];
+  __shared__ double s_sum;
+  const float* sr = s + (size_t)blockIdx.x * d;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) mx = fmaxf(mx, sr[c]);
+  mx = block_max(mx, red);
+  for (int c = threadIdx.x; c < d; c += blockDim.x) e_s[c] = exp((double)sr[c] - (double)mx);
+  __syncthreads();
+  if (threadIdx.x == 0) s_sum = pairwise_sum<10, double>(e_s, d);
+  __syncthreads();
+  const double sum = s_sum;
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    out[(size_t)blockIdx.x * d + c] = (float)(e_s[c] / sum);
+}
+
+int grid_of(size_t n) { return (int)((n + 255) / 256); }
+
+}  // namespace
+
+// largest row width of the per-row kernels (shared-memory bound)
+constexpr int kMaxRowWidth = 24576;
+
+cudaError_t launch_online_softmax_update(const float* m, const float* l, const float* acc,
+                                         const float* scores, const float* v, int rows, int cols,
+                                         int d, float* m_out, float* l_out, float* acc_out,
+                                         cudaStream_t st) {
+  const size_t sm = (size_t)cols * 4;
+  cudaFuncSetAttribute(online_softmax_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm);
+  note_launch();
+  online_softmax_update_kernel<<<rows, kRowThreads, sm, st>>>(m, l, acc, scores, v, cols, d, m_out,
+                                                              l_out, acc_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_online_softmax_finalize(const float* acc, const float* l, int rows, int d,
+                                           float* out, uint32_t* status, cudaStream_t st) {
+  note_launch();
+  online_softmax_finalize_kernel<<<grid_of((size_t)rows * d), 256, 0, st>>>(acc, l, rows, d, out,
+                                                                            status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_entry(const float* old, const float* o, size_t tile, int order, int valid,
+                                float* stack, cudaStream_t st) {
+  note_launch();
+  update_entry_kernel<<<grid_of(tile), 256, 0, st>>>(old, o, tile, order, valid, stack);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_forecast_entry(const float* stack, size_t tile, int n_orders, const float* coef,
+                                  float* out, cudaStream_t st) {
+  Coef c{};
+  for (int k = 0; k < n_orders && k < 8; ++k) c.c[k] = coef[k];
+  note_launch();
+  forecast_entry_kernel<<<grid_of(tile), 256, 0, st>>>(stack, tile, n_orders, c, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mean_pool(const float* x, int n, int d, int pool, float* out, cudaStream_t st) {
+  const int blocks = (n + pool - 1) / pool;
+  note_launch();
+  mean_pool_kernel<<<grid_of((size_t)blocks * d), 256, 0, st>>>(x, n, d, pool, blocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rms_norm(const float* x, const float* w, int n, int d, double eps, float* out,
+                            cudaStream_t st) {
+  const size_t sm = (size_t)d * 8;
+  cudaFuncSetAttribute(rms_norm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  note_launch();
+  rms_norm_kernel<<<n, kRowThreads, sm, st>>>(x, w, d, eps, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rope(const float* x, const float* cs, const float* sn, int n, int d, float* out,
+                        cudaStream_t st) {
+  note_launch();
+  rope_kernel<<<grid_of((size_t)n * (d / 2)), 256, 0, st>>>(x, cs, sn, n, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_softmax(const float* s, int n, int d, float* out, cudaStream_t st) {
+  const size_t sm = (size_t)d * 8;
+  cudaFuncSetAttribute(row_softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  note_launch();
+  row_softmax_kernel<<<n, kRowThreads, sm, st>>>(s, d, out);
+  return cudaGetLastError();
+}
+
+int max_row_width() { return kMaxRowWidth; }
+
+}  // namespace fo

@@ -197,9 +197,15 @@ def test_gpu_policy_errors():
         fo.generate_masks_heads(q, q, pool_n=1, n_text=0, tau_q=0.2, tau_kv=float("nan"))
     with pytest.raises(fo.ParameterError):  # text fills every compressed row
         fo.generate_masks_heads(q, q, pool_n=1, n_text=512, tau_q=0.2, tau_kv=0.1)
+    # the per-head reference signature runs the policy stages at any block
+    # size (policy.py:196-234); with no text both scores are 0, every prefix sum
+    # 0 <= tau * 0 holds and the reference caches every block
+    cb, sb = fo.generate_masks(np.zeros((512, 64), np.float32), np.zeros((512, 64), np.float32),
+                               b_q=64, b_k=64, pool_n=1, n_text=0, tau_q=0.1, tau_kv=0.1)
+    assert cb.shape == (8,) and sb.shape == (8, 8) and not cb.any() and not sb.any()
     with pytest.raises(fo.ParameterError):
         fo.generate_masks(np.zeros((512, 64), np.float32), np.zeros((512, 64), np.float32), b_q=64,
-                          b_k=64, pool_n=1, n_text=0, tau_q=0.1, tau_kv=0.1)
+                          b_k=32, pool_n=1, n_text=0, tau_q=0.1, tau_kv=0.1)
 
 
 @pytest.mark.gpu
