@@ -26,6 +26,19 @@
 #ifndef FO_GO_EVICT_FIRST
 #define FO_GO_EVICT_FIRST 1
 #endif
+#ifndef FO_GO_EF_LOAD
+#define FO_GO_EF_LOAD FO_GO_EVICT_FIRST  // dispatch bias loads evict-first
+#endif
+#ifndef FO_GO_EF_STORE
+#define FO_GO_EF_STORE FO_GO_EVICT_FIRST  // dispatch out stores evict-first
+#endif
+#ifndef FO_GO_EL_OPS
+#define FO_GO_EL_OPS 1  // dispatch o / W operand loads evict-last
+#endif
+
+#ifndef FO_GO_PF
+#define FO_GO_PF 1  // GEMM-O dispatch: bias L2 prefetch distance in jobs
+#endif
 
 namespace fo {
 namespace gemm {
@@ -42,8 +55,18 @@ constexpr int NTHREADS = 256;
 // bias-loader warp, the epilogue and the TMA store
 constexpr int D_BN = 256;
 constexpr int D_STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // 48 KB
-constexpr int D_STAGES = 3;
-constexpr int BIAS_SLOTS = 8;  // max slots (8 x 8 KB at order 0, 4 x 16 KB at orders >= 1)
+#ifndef FO_GO_DST
+#define FO_GO_DST 3
+#endif
+#ifndef FO_GO_RING
+#define FO_GO_RING 4  // bias ring in 16 KB units
+#endif
+#ifndef FO_GO_OST
+#define FO_GO_OST 2  // output staging buffers
+#endif
+constexpr int D_STAGES = FO_GO_DST;
+constexpr int BIAS_SLOTS = 2 * FO_GO_RING;  // max slots (8 KB each at order 0, 16 KB at orders >= 1)
+constexpr int OST = FO_GO_OST;
 constexpr int BIAS_ORDER_BYTES = BM * 32 * 2;  // 8 KB
 constexpr int BIAS_SLOT_BYTES = 2 * BIAS_ORDER_BYTES;
 
@@ -53,13 +76,12 @@ struct Bars {
   uint64_t bfull[BIAS_SLOTS], bempty[BIAS_SLOTS];
   uint32_t tmem_base;
 };
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + (int)sizeof(Bars);
 // output chunks are staged separately (double-buffered) so a bias slot is free
 // as soon as the epilogue has read it, not when the chunk's store has read it
 constexpr int OUT_STAGE_BYTES = BM * 32 * 2;  // 8 KB, SW64 like the bias chunks
-constexpr int BIAS_RING_BYTES = 4 * BIAS_SLOT_BYTES;  // 64 KB
+constexpr int BIAS_RING_BYTES = FO_GO_RING * BIAS_SLOT_BYTES;  // 64 KB
 constexpr int SMEM_BYTES_D = D_STAGES * D_STAGE_BYTES + BIAS_RING_BYTES +
-                             2 * OUT_STAGE_BYTES + 1024 + (int)sizeof(Bars);
+                             OST * OUT_STAGE_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES_D <= 232448, "dispatch shared memory over the sm_100 limit");
 
 // empty_count: consumers that release a stage (2 when the A tile is multicast
@@ -495,7 +517,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* ring = smem + ST * SB;  // dispatch bias / output chunks
   uint8_t* ostage = ring + (UPDATE ? 0 : BIAS_RING_BYTES);  // dispatch out chunks
-  Bars* bars = reinterpret_cast<Bars*>(ostage + (UPDATE ? 0 : 2 * OUT_STAGE_BYTES));
+  Bars* bars = reinterpret_cast<Bars*>(ostage + (UPDATE ? 0 : OST * OUT_STAGE_BYTES));
   const int warp = warp_id(), lane = lane_id();
   const int rank = MC ? (int)cluster_ctarank() : 0;
   if (warp == 0 && lane == 0) {
@@ -575,6 +597,20 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                 uint8_t* st = smem + rg.s * SB;
                 mbar_arrive_expect_tx(&bars->full[rg.s],
                                       A_BYTES + (mine ? (two ? 2 : 1) * B_BYTES : 0));
+#if FO_GO_EL_OPS
+                const uint64_t pol = l2_evict_last_policy();
+                if (MC)
+                  tma_load_2d_mc_hint(st + rank * (A_BYTES / 2), src, &bars->full[rg.s],
+                                      h * 128 + kk * BK, row0 + rank * (BM / 2), 0x3, pol);
+                else
+                  tma_load_2d_hint(st, src, &bars->full[rg.s], h * 128 + kk * BK, row0, pol);
+                if (mine)
+                  tma_load_2d_hint(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
+                                   nb * TBN, pol);
+                if (two)
+                  tma_load_2d_hint(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s],
+                                   h * 128 + kk * BK, nb * TBN + BN, pol);
+#else
                 if (MC)
                   tma_load_2d_mc(st + rank * (A_BYTES / 2), src, &bars->full[rg.s],
                                  h * 128 + kk * BK, row0 + rank * (BM / 2), 0x3);
@@ -585,6 +621,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                 if (two)
                   tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
                               nb * TBN + BN);
+#endif
               }
               __syncwarp();
               rg.next();
@@ -655,14 +692,19 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       if (!job(w, i, nb, d)) continue;
       const int ns = staged_orders(i);
       const int nch = tile_cols(nb) / 32;
-      const int wn = w + jstep;
-      int i2, nb2, d2;
-      if (wn < n_jobs && job(wn, i2, nb2, d2) && elect_one()) {
-        const int ns2 = staged_orders(i2);
-        for (int dd = 0; dd < ns2; ++dd)
-          for (int c = 0; c < tile_cols(nb2) / 32; ++c)
-            tma_prefetch_l2_2d(&cm, nb2 * TBN + c * 32, dd * p.S + i2 * BM);
-      }
+      // L2 prefetch FO_GO_PF jobs ahead: DRAM requests in flight beyond the ring
+      auto prefetch = [&](int wn) {
+        int i2, nb2, d2;
+        if (wn < n_jobs && job(wn, i2, nb2, d2) && elect_one()) {
+          const int ns2 = staged_orders(i2);
+          for (int dd = 0; dd < ns2; ++dd)
+            for (int c = 0; c < tile_cols(nb2) / 32; ++c)
+              tma_prefetch_l2_2d(&cm, nb2 * TBN + c * 32, dd * p.S + i2 * BM);
+        }
+      };
+      if (w == jstart)
+        for (int k = 1; k < FO_GO_PF; ++k) prefetch(w + k * jstep);
+      prefetch(w + FO_GO_PF * jstep);
       __syncwarp();
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&bars->bempty[rb.s], rb.ph ^ 1);
@@ -670,7 +712,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           uint8_t* slot = ring + rb.s * bias_slot_bytes;
           mbar_arrive_expect_tx(&bars->bfull[rb.s], ns * BIAS_ORDER_BYTES);
           for (int dd = 0; dd < ns; ++dd)
-#if FO_GO_EVICT_FIRST
+#if FO_GO_EF_LOAD
             tma_load_2d_hint(slot + dd * BIAS_ORDER_BYTES, &cm, &bars->bfull[rb.s],
                              nb * TBN + c * 32, dd * p.S + i * BM, l2_evict_first_policy());
 #else
@@ -756,6 +798,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           if (hasA) {
             tmem_ld32(tA + c * 32, ua);
             tmem_ld_wait();
+            gemm::reg_fence(ua);
           } else {
 #pragma unroll
             for (int k = 0; k < 32; ++k) ua[k] = 0u;
@@ -823,17 +866,17 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           __syncwarp();
           if (lane == 0) {
             uint8_t* src = ostage + ob * OUT_STAGE_BYTES + q4 * (OUT_STAGE_BYTES / 4);
-#if FO_GO_EVICT_FIRST
+#if FO_GO_EF_STORE
             tma_store_2d_hint(&om, src, nb * TBN + c * 32, i * BM + q4 * 32,
                               l2_evict_first_policy());
 #else
             tma_store_2d(&om, src, nb * TBN + c * 32, i * BM + q4 * 32);
 #endif
             bulk_commit();
-            bulk_wait_read<1>();  // this warp's quarter of the other buffer is free
+            bulk_wait_read<OST - 1>();  // this warp's quarter of the other buffer is free
           }
           __syncwarp();
-          ob ^= 1;
+          ob = ob + 1 == OST ? 0 : ob + 1;
         }
         ++t;
       }

@@ -18,26 +18,18 @@ ap.add_argument("--ratios", default="0.0,0.25,0.75,0.9")
 ap.add_argument("--orders", default="0,1")
 ap.add_argument("--ops", default="q,disp,upd")
 ap.add_argument("--seq", type=int, default=33024)
+ap.add_argument("--eager", action="store_true", help="time Python calls, not a CUDA graph")
 a = ap.parse_args()
 S, H, dm, T = a.seq, 24, 3072, 128
 t = S // T
 ops = set(a.ops.split(","))
 
 
+from tools.timing import eager_time, graph_time  # noqa: E402
+
+
 def timeit(fn, reps=10, trials=5):
-    for _ in range(3):
-        fn()
-    torch.cuda.synchronize()
-    res = []
-    for _ in range(trials):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        res.append(e0.elapsed_time(e1) / reps)
-    return float(np.median(res))
+    return (eager_time if a.eager else graph_time)(fn, reps=reps, trials=trials)
 
 
 g = torch.Generator(device="cuda").manual_seed(0)

@@ -27,17 +27,14 @@ from bench import random_masks  # noqa: E402
 T = 128
 
 
+EAGER = False
+
+
 def timeit(fn, warm=2, reps=5):
-    for _ in range(warm):
-        fn()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    """median ms per call: a CUDA graph of `reps` calls (tools/timing.py)"""
+    from tools.timing import eager_time, graph_time
+
+    return (eager_time if EAGER else graph_time)(fn, reps=reps, trials=5, warm=warm)
 
 
 def attention_sweep(S, H, points, seed=0):
@@ -125,13 +122,17 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--parts", default="attn,flux,gemm", help="subset of attn,flux,gemm")
+    ap.add_argument("--eager", action="store_true", help="time Python calls, not CUDA graphs")
     a = ap.parse_args()
+    global EAGER
+    EAGER = a.eager
     parts = set(a.parts.split(","))
     pts = [("dense", 0.0, 0.0)]
     pts += [("FC", c, 0.0) for c in (0.1, 0.3, 0.5, 0.8)]
     pts += [("BSS", 0.0, s) for s in (0.1, 0.3, 0.5, 0.8)]
     pts += [("FC+BSS", c, s) for c, s in ((0.25, 0.5), (0.5, 0.6), (0.5, 0.8))]
-    res = {"device": torch.cuda.get_device_name()}
+    res = {"device": torch.cuda.get_device_name(),
+           "timing": "eager Python calls" if EAGER else "CUDA graph of 5 calls, median of 5 replays"}
     if "attn" in parts:
         res["attention_c4"] = attention_sweep(33024, 24, pts)
     flux = [("BSS", 0.0, s) for s in (0.0, 0.1, 0.3, 0.5, 0.7, 0.9)]
