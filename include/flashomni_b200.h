@@ -174,6 +174,17 @@ FO_API int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bia
                        int seq, int heads, int head_dim, int d_model, int order_d,
                        const float* coef, const void* plan_ws, void* out, void* stream);
 
+/* fo_gemm_o_dispatch restricted to query blocks [block_begin, block_end) (rows
+ * 128*block_begin .. of `out`; other rows untouched) on at most max_sms SMs (0 =
+ * all): the row-chunked dispatch the multi-GPU step overlaps with the
+ * all-reduce of the previous chunk. BOUNDS for a range outside
+ * [0, rows). */
+FO_API int fo_gemm_o_dispatch_rows(const void* o, const void* w_outt, const void* bias,
+                                   const int32_t* orders, int seq, int heads, int head_dim,
+                                   int d_model, int order_d, const float* coef, const void* plan_ws,
+                                   int block_begin, int block_end, int max_sms, void* out,
+                                   void* stream);
+
 /* Stale-symbol check (gemm.py:201-209): STATE if the decoded cache bits differ. */
 FO_API int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
                           int pool_n, uint32_t* status, void* stream);

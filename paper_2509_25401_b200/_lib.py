@@ -49,6 +49,7 @@ SIGNATURES = {
     "fo_gemm_q": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _F, _P, _I, _P, _P],
     "fo_gemm_o_update": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "fo_gemm_o_dispatch": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "fo_gemm_o_dispatch_rows": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P],
     "fo_check_active_match": [_P, _P, _I, _I, _I, _P, _P],
     "fo_policy_workspace_bytes": [_I, _I, _I],
     "fo_generate_masks": [_P, _P, _I, _I, _I, _I, _D, _D, _D, _I, _P, _P, _P, _SZ, _P],

@@ -453,6 +453,8 @@ static int gemm_o_common(const void* o, const void* cache, const void* w_outt, i
   p.H = heads;
   p.t_q = t_q;
   p.order_d = order_d;
+  p.i_begin = 0;
+  p.i_end = t_q;
   p.hmask = pv.hmask;
   p.orders = pv.orders;
   for (int d = 0; d < 4; ++d) p.coef[d] = 0.f;
@@ -494,6 +496,14 @@ int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int s
 int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, const int32_t* orders,
                        int seq, int heads, int head_dim, int d_model, int order_d,
                        const float* coef, const void* plan_ws, void* out, void* stream) {
+  return fo_gemm_o_dispatch_rows(o, w_outt, bias, orders, seq, heads, head_dim, d_model, order_d,
+                                 coef, plan_ws, 0, ceil_div_d(seq, kTile), 0, out, stream);
+}
+
+int fo_gemm_o_dispatch_rows(const void* o, const void* w_outt, const void* bias,
+                            const int32_t* orders, int seq, int heads, int head_dim, int d_model,
+                            int order_d, const float* coef, const void* plan_ws, int block_begin,
+                            int block_end, int max_sms, void* out, void* stream) {
   GemmOParams p;
   CUtensorMap am, cm, wm;
   int rc = gemm_o_common(o, nullptr, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p,
@@ -502,7 +512,14 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
   if (!orders || !bias) return fail(FO_ERR_STATE, "dispatch projection requires the update-step bias");
   if (!coef) return fail(FO_ERR_PARAM, "gemm_o_dispatch: coef is NULL");
   if (!out) return fail(FO_ERR_PARAM, "gemm_o_dispatch: out is NULL");
+  if (block_begin < 0 || block_end > p.t_q || block_begin > block_end)
+    return fail(FO_ERR_BOUNDS, "gemm_o_dispatch: block range [%d, %d) outside [0, %d)", block_begin,
+                block_end, p.t_q);
+  if (max_sms < 0 || max_sms == 1) return fail(FO_ERR_PARAM, "gemm_o_dispatch: max_sms=%d", max_sms);
+  if (block_begin == block_end) return FO_OK;
   p.update = 0;
+  p.i_begin = block_begin;
+  p.i_end = block_end;
   p.orders = orders;
   for (int d = 0; d <= order_d; ++d) p.coef[d] = coef[d];
   p.out = static_cast<__nv_bfloat16*>(out);
@@ -517,7 +534,7 @@ int fo_gemm_o_dispatch(const void* o, const void* w_outt, const void* bias, cons
     return rc;
   // o moves in half tiles (64 rows), each multicast to both CTAs of a cluster
   if ((rc = make_map(&am, o, seq, (uint64_t)heads * kTile, 64, "o"))) return rc;
-  launch_gemm_o(am, bm, wm, om, p, num_sms(), (cudaStream_t)stream);
+  launch_gemm_o(am, bm, wm, om, p, max_sms > 0 ? max_sms : (1 << 30), (cudaStream_t)stream);
   return check_launch("gemm_o_dispatch");
 }
 

@@ -159,8 +159,18 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 
 // launch a persistent kernel as 2-CTA clusters, as many as can be co-resident
 template <typename Kernel, typename... Args>
+static void launch_pair_clusters_max(Kernel kernel, int smem, int* grid_cache, int max_ctas,
+                                     cudaStream_t stream, Args... args);
+template <typename Kernel, typename... Args>
 static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaStream_t stream,
                                  Args... args) {
+  launch_pair_clusters_max(kernel, smem, grid_cache, 1 << 30, stream, args...);
+}
+// max_ctas < the co-resident grid leaves SMs free for a concurrent kernel (the
+// all-reduce of the previous row chunk)
+template <typename Kernel, typename... Args>
+static void launch_pair_clusters_max(Kernel kernel, int smem, int* grid_cache, int max_ctas,
+                                     cudaStream_t stream, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -182,7 +192,7 @@ static void launch_pair_clusters(Kernel kernel, int smem, int* grid_cache, cudaS
       clusters = sms / 2;
     *grid_cache = 2 * std::min(clusters, sms / 2);
   }
-  cfg.gridDim = dim3(*grid_cache);
+  cfg.gridDim = dim3(std::max(2, std::min(*grid_cache, max_ctas & ~1)));
   note_launch();
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
@@ -538,7 +548,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   auto tile_cols = [&](int nb) { return min(TBN, p.dm - nb * TBN); };
   const int nord = UPDATE ? p.order_d + 1 : 1;
   const int ncb = (nbn + 1) >> 1;  // dispatch: n-tile pairs per block (one per cluster job)
-  const int n_jobs = MC ? p.t_q * ncb : p.t_q * nbn * nord;
+  const int n_jobs = MC ? (p.i_end - p.i_begin) * ncb : p.t_q * nbn * nord;
   const int jstart = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int jstep = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const unsigned long long all_heads = (p.H >= 64) ? ~0ull : ((1ull << p.H) - 1);
@@ -549,8 +559,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   // n-tile is past the end (it still loads its half of the shared o tile).
   auto job = [&](int w, int& i, int& nb, int& d) -> bool {
     if (MC) {
-      i = w / ncb;
-      nb = 2 * (w - i * ncb) + rank;
+      const int ib = w / ncb;
+      i = p.i_begin + ib;
+      nb = 2 * (w - ib * ncb) + rank;
       d = 0;
       return nb < nbn;
     }
@@ -1152,9 +1163,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
 }
 
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
-                   const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream) {
+                   const CUtensorMap& om, const GemmOParams& p, int max_ctas, cudaStream_t stream) {
   static int grid_d = 0;
-  launch_pair_clusters(gemm_o_kernel<false>, gemm::SMEM_BYTES_D, &grid_d, stream, am, cm, wm, om, p);
+  launch_pair_clusters_max(gemm_o_kernel<false>, gemm::SMEM_BYTES_D, &grid_d, max_ctas, stream, am,
+                           cm, wm, om, p);
 }
 
 void launch_gemm_o_update(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,

@@ -206,6 +206,7 @@ void launch_gemm_q2(const CUtensorMap& xm, const CUtensorMap& wm, const CUtensor
 struct GemmOParams {
   int S, dm, H, t_q, order_d;
   int update;                            // 1: update (writes bias), 0: dispatch (reads bias)
+  int i_begin, i_end;                    // dispatch: query-block range [i_begin, i_end)
   const unsigned long long* hmask;       // [t_q]
   const int* orders;                     // [t_q]
   float coef[4];                         // dispatch forecast coefficients c_d
@@ -215,7 +216,7 @@ struct GemmOParams {
 };
 // dispatch (K4): 2-CTA clusters, bias chunks through a TMA ring
 void launch_gemm_o(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
-                   const CUtensorMap& om, const GemmOParams& p, int grid, cudaStream_t stream);
+                   const CUtensorMap& om, const GemmOParams& p, int max_ctas, cudaStream_t stream);
 // update (K5): 2-CTA clusters; cm / bm are 3-D [order+1][S][cols] maps
 void launch_gemm_o_update(const CUtensorMap& am, const CUtensorMap& cm, const CUtensorMap& wm,
                           const CUtensorMap& om, const CUtensorMap& bm, const GemmOParams& p,

@@ -271,6 +271,7 @@ class _Layer:
                                  device=device)
         self.ready = False
         self.graphs = {}
+        self.group = None
 
     # ------------------------------------------------------------------ phases
     def update(self, x, t_step, status):
@@ -299,8 +300,18 @@ class _Layer:
         computed = (self.sb.to(torch.int64).sum(dim=2) * cb).sum()
         active_rows = (cb * self.rows).sum()
         orders = self.bias.orders.to(torch.int64)
+        if self.group is not None:
+            # a rank without cached heads in block i has orders 0 there; the
+            # others agree (same push history), so the layer's orders are the
+            # max over ranks and the bias work is counted once per block, as
+            # the unsharded reference counts it (gemm.py:164-166, 218-224)
+            import torch.distributed as dist
+
+            dist.all_reduce(orders, op=dist.ReduceOp.MAX, group=self.group)
         n_ord = torch.clamp(orders, max=self.cfg.order_d + 1)
         bias_disp = (n_ord * self.rows).sum()
+        if self.group is not None and dist.get_rank(self.group) != 0:
+            bias_disp = bias_disp * 0  # identical on every rank: summed once by the all-reduce
         ncached = self.H - cb.sum(dim=0)
         bias_upd = (ncached * torch.clamp(orders - 1, min=0) * self.rows).sum()
         return torch.stack([computed, active_rows, bias_disp, bias_upd])
@@ -350,6 +361,8 @@ class Engine:
         self.heads_idx = shard_heads(config.heads, world, rank)
         self.layers = [_Layer(config, lp, self.heads_idx, self.device)
                        for lp in self.workload.layer_params]
+        for layer in self.layers:
+            layer.group = group
         self.x_buf = torch.zeros(config.n_tokens, config.d_model, dtype=torch.bfloat16,
                                  device=self.device)
         self.status = Status(device=self.device)

@@ -242,9 +242,13 @@ def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE
 
 
 def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, order_d, *, b_q=TILE,
-                         counters=None, out=None, stream=None, status=None, check=True, plan=None):
+                         counters=None, out=None, stream=None, status=None, check=True, plan=None,
+                         blocks=None, max_sms=0):
     """Dispatch-step output projection (gemm.py:178-229): active heads plus the
-    forecast of the cached-head bias stacks."""
+    forecast of the cached-head bias stacks. blocks=(b0, b1) computes only the
+    rows of query blocks [b0, b1) (the rest of `out` is untouched) on at most
+    max_sms SMs (0 = all): the row chunks the multi-GPU step overlaps with the
+    all-reduce (pipeline.dispatch_step)."""
     require_cuda()
     if b_q != TILE:
         raise ParameterError(f"the sm_100a kernels tile blocks of {TILE} tokens")
@@ -277,14 +281,16 @@ def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, o
         out = torch.empty(n, dm, dtype=torch.bfloat16, device=o.device)
     else:
         check_out(out, "out", (n, dm), device=o.device)
-    _lib.call("fo_gemm_o_dispatch", o.data_ptr(), w.t.data_ptr(), bias.stacks.data_ptr(),
+    b0, b1 = (0, t_q) if blocks is None else (int(blocks[0]), int(blocks[1]))
+    _lib.call("fo_gemm_o_dispatch_rows", o.data_ptr(), w.t.data_ptr(), bias.stacks.data_ptr(),
               bias.orders.data_ptr(), n, heads, TILE, dm, min(order_d, bias.order_d),
-              ctypes.addressof(coef), plan.ptr(), out.data_ptr(), stream_ptr(stream))
+              ctypes.addressof(coef), plan.ptr(), b0, b1, int(max_sms), out.data_ptr(),
+              stream_ptr(stream))
     if counters is not None:
-        counters.o_macs_dense += heads * n * TILE * dm
+        counters.o_macs_dense += heads * sum(min(TILE, n - i * TILE) for i in range(b0, b1)) * TILE * dm
         hm = plan.hmask()
         ords = bias.orders.cpu().numpy()
-        for i in range(t_q):
+        for i in range(b0, b1):
             rows = min(TILE, n - i * TILE)
             counters.o_macs_actual += bin(int(hm[i])).count("1") * rows * TILE * dm
             if ords[i]:

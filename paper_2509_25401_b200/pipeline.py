@@ -107,10 +107,58 @@ def update_step(state, x, symbols_next, order_d, *, group=None, check=True, poli
     return _allreduce(out, group)
 
 
+_COMM = {}
+
+
+def _comm_stream(device):
+    if device not in _COMM:
+        _COMM[device] = torch.cuda.Stream(device=device)
+    return _COMM[device]
+
+
+def _dispatch_out_allreduce(o, p, state, elapsed_k, interval_n, order_d, out, group, chunks, check,
+                            comm_sms):
+    """GEMM-O dispatch in `chunks` row chunks, each chunk's all-reduce issued on
+    a side stream as soon as its rows are written, so the transfer of chunk c
+    overlaps the projection of chunk c + 1 (the reduction is per row, so the
+    chunked sum equals the whole one). comm_sms SMs are left to the
+    collective's kernels while the projection of the next chunk runs."""
+    import torch.distributed as dist
+
+    n = o.shape[0]
+    t_q = ceil_div(n, TILE)
+    if out is None:
+        out = torch.empty(n, p.w_out.d_model, dtype=torch.bfloat16, device=o.device)
+    chunks = max(1, min(int(chunks), t_q))
+    bounds = [t_q * c // chunks for c in range(chunks + 1)]
+    main = torch.cuda.current_stream(o.device)
+    comm = _comm_stream(o.device)
+    sms = 0
+    if chunks > 1 and comm_sms > 0:
+        sms = max(2, torch.cuda.get_device_properties(o.device).multi_processor_count - comm_sms)
+    works = []
+    for c in range(chunks):
+        b0, b1 = bounds[c], bounds[c + 1]
+        project_out_dispatch(o, p.w_out, state.symbols, state.bias, elapsed_k, interval_n, order_d,
+                             out=out, blocks=(b0, b1), max_sms=sms, check=check and c == 0)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        comm.wait_event(ev)
+        with torch.cuda.stream(comm):
+            works.append(dist.all_reduce(out[b0 * TILE:min(b1 * TILE, n)], group=group,
+                                         async_op=True))
+    for w in works:
+        w.wait()
+    main.wait_stream(comm)
+    return out
+
+
 def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check=True, fill=None,
-                  bufs=None):
+                  bufs=None, chunks=1, comm_sms=0):
     """Sparse execution against the governing symbols (pipeline.py:291-326).
-    bufs: optional dict of preallocated q/k/v/o/out tensors (graph capture)."""
+    bufs: optional dict of preallocated q/k/v/o/out tensors (graph capture).
+    With a process group, chunks > 1 overlaps GEMM-O row chunks with the
+    all-reduce of the previous chunk (_dispatch_out_allreduce)."""
     if state.symbols is None or state.bias is None:
         raise StateError("dispatch step before any update step")
     x = as_device(x, torch.bfloat16, "x")
@@ -121,6 +169,9 @@ def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check
     k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"), check=False)
     o = sparse_attention(q, k, v, state.symbols, state.cache, None, elapsed_k, interval_n, order_d,
                          mode="bias", fill=fill, out=b.get("o"), check=check)
+    if group is not None and chunks > 1:
+        return _dispatch_out_allreduce(o, p, state, elapsed_k, interval_n, order_d, b.get("out"),
+                                       group, chunks, check, comm_sms)
     out = project_out_dispatch(o, p.w_out, state.symbols, state.bias, elapsed_k, interval_n,
                                order_d, out=b.get("out"), check=check)
     return _allreduce(out, group)
