@@ -36,6 +36,10 @@ CONFIGS = {
     "c4": dict(name="C4 HunyuanVideo attention layer, 33K tokens", seq=33024, heads=24, d_model=3072),
     "c1": dict(name="C1 single DiT attention layer, 4096 tokens", seq=4096, heads=24, d_model=3072),
     "c2": dict(name="C2 FLUX.1-dev joint attention, 4608 tokens", seq=4608, heads=24, d_model=3072),
+    # C5: the C4 layer as a block stack (layer l's output is layer l+1's input);
+    # 4 layers [choice], --layers overrides
+    "c5": dict(name="C5 HunyuanVideo DiT block stack, 33K tokens", seq=33024, heads=24,
+               d_model=3072, layers=4),
 }
 
 
@@ -56,6 +60,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also sweep sparsity (extra JSON key)")
+    ap.add_argument("--layers", type=int, default=None, help="layers in the stack (c5: 4)")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch the operators from Python each step instead of replaying "
+                         "their CUDA graphs")
     return ap.parse_args()
 
 
@@ -220,16 +228,21 @@ def run_reference(args, cfg, rank, world):
                 parts_sum[k2] = parts_sum.get(k2, 0.0) + v2
     finally:
         L.close()
-    v = total * 1e3
+    nl = layers_of(args, cfg)
+    v = total * 1e3 * nl
     assert pairs == int(L.pairs_per_unit.sum()), "the K slices must cover the layer exactly once"
     sample = (f"the whole layer step, as {args.steps} interleaved slices (one per timed step; "
               f"{pairs} attention pairs, all GEMM-Q tiles and GEMM-O row blocks); attention "
               f"backend {L.backend} on {L.workers} worker processes, GEMMs numpy/OpenBLAS")
+    if nl > 1:
+        sample += f"; one layer measured, x {nl} layers of the stack (same shapes and sparsity)"
+    layers = [dict(cb=cache_bits, sb=skip_bits)] * nl
+    parts_sum = {k: x * nl for k, x in parts_sum.items()}
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1) tensors, random symbols)",
-            "config": config_json(args, cfg, world, cache_bits, skip_bits),
+            "config": config_json(args, cfg, world, layers),
             "breakdown_ms": {k: round(x * 1e3, 3) for k, x in parts_sum.items()},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_threads(),
                              "kind": L.kind, "sample": sample},
@@ -238,17 +251,25 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_json(args, cfg, world, cache_bits, skip_bits):
+def layers_of(args, cfg):
+    return args.layers if args.layers is not None else cfg.get("layers", 1)
+
+
+def config_json(args, cfg, world, layers):
     H, t = cfg["heads"], cfg["seq"] // T
-    computed = int(sum(skip_bits[h][cache_bits[h]].sum() for h in range(H)))
-    return {"workload": cfg["name"], "seq": cfg["seq"], "heads": H, "head_dim": T,
+    computed = sum(int(sum(ly["sb"][h][ly["cb"][h]].sum() for h in range(H))) for ly in layers)
+    L = len(layers)
+    extra = {"layers": L} if L > 1 else {}
+    return {"workload": cfg["name"], **extra, "seq": cfg["seq"], "heads": H, "head_dim": T,
             "d_model": cfg["d_model"], "b_q": T, "b_k": T, "pool_n": 1,
             "cached_ratio": args.cached, "kv_skip_ratio": args.skip,
-            "pair_sparsity": round(1 - computed / (H * t * t), 4),
+            "pair_sparsity": round(1 - computed / (L * H * t * t), 4),
             "interval_n": args.interval, "order_d": args.order, "elapsed_k": args.elapsed,
             "symbols": "random (verify.py:29-44 rule), seed %d" % args.seed,
             "parallelism": "heads/%d" % world if world > 1 else "single GPU",
-            "l2": "inputs larger than L2 (x/q/k/v/o 203 MB each), no flush"}
+            "l2": "inputs larger than L2 (x/q/k/v/o 203 MB each), no flush",
+            "launch": ("eager Python calls" if getattr(args, "eager", True) else
+                       "each operator replayed as a CUDA graph (as the engine runs steps)")}
 
 
 # ---------------------------------------------------------------------------
@@ -266,8 +287,8 @@ def run_b200(args, cfg, rank, world):
     group = dist.group.WORLD if world > 1 else None
     S, H, dm = cfg["seq"], cfg["heads"], cfg["d_model"]
     t = S // T
+    L = layers_of(args, cfg)
     rng = np.random.default_rng(args.seed)
-    cache_bits, skip_bits = random_masks(rng, H, t, args.cached, args.skip)
     heads = fo.shard_heads(H, world, rank)
     Hl = len(heads)
     g = torch.Generator(device=dev).manual_seed(args.seed)
@@ -275,47 +296,97 @@ def run_b200(args, cfg, rank, world):
     def randn(*shape, scale=1.0):
         return torch.randn(*shape, device=dev, generator=g) * scale
 
-    # weights (reference init, pipeline.py:145-159), packed once
-    params = fo.LayerParams.from_reference(
-        randn(H, dm, T, scale=dm ** -0.5), randn(H, dm, T, scale=dm ** -0.5),
-        randn(H, dm, T, scale=dm ** -0.5), 1 + 0.05 * randn(H, T), 1 + 0.05 * randn(H, T),
-        randn(H, T, dm, scale=T ** -0.5), heads=heads)
     x = randn(S, dm).bfloat16()
-    k, v = fo.project_kv(x, params)
-    sym = fo.encode_symbols(cache_bits[heads], skip_bits[heads], 1)
     dense_sym = fo.encode_symbols(np.ones((Hl, t), bool), np.ones((Hl, t, t), bool), 1)
-    cache = fo.FeatureCache(Hl, t, args.order, seq=S)
-    for _ in range(args.order + 1):
-        cache.push(randn(S, Hl, T).bfloat16())
-    o_upd = randn(S, Hl, T).bfloat16()
-    _, bias = fo.project_out_update(o_upd, params.w_out, sym, cache, args.order)
-    _, bias_dense = fo.project_out_update(o_upd, params.w_out, dense_sym, cache, args.order)
+    layers = []
+    for li in range(L):
+        # layer li: its own symbols (the next draws of the same rng), weights
+        # (reference init, pipeline.py:145-159, packed once), cache and bias
+        cb_l, sb_l = random_masks(rng, H, t, args.cached, args.skip)
+        params = fo.LayerParams.from_reference(
+            randn(H, dm, T, scale=dm ** -0.5), randn(H, dm, T, scale=dm ** -0.5),
+            randn(H, dm, T, scale=dm ** -0.5), 1 + 0.05 * randn(H, T), 1 + 0.05 * randn(H, T),
+            randn(H, T, dm, scale=T ** -0.5), heads=heads)
+        k, v = fo.project_kv(x, params)
+        sym = fo.encode_symbols(cb_l[heads], sb_l[heads], 1)
+        cache = fo.FeatureCache(Hl, t, args.order, seq=S)
+        for _ in range(args.order + 1):
+            cache.push(randn(S, Hl, T).bfloat16())
+        o_upd = randn(S, Hl, T).bfloat16()
+        _, bias = fo.project_out_update(o_upd, params.w_out, sym, cache, args.order)
+        _, bias_dense = fo.project_out_update(o_upd, params.w_out, dense_sym, cache, args.order)
+        layers.append(dict(params=params, k=k, v=v, sym=sym, cache=cache, bias=bias,
+                           bias_dense=bias_dense, cb=cb_l, sb=sb_l))
+    cache_bits, skip_bits = layers[0]["cb"], layers[0]["sb"]
+    params, k, v, cache = (layers[0][n] for n in ("params", "k", "v", "cache"))
+    sym, bias, bias_dense = layers[0]["sym"], layers[0]["bias"], layers[0]["bias_dense"]
     q = torch.empty(S, Hl, T, dtype=torch.bfloat16, device=dev)
     o = torch.empty_like(q)
-    out = torch.empty(S, dm, dtype=torch.bfloat16, device=dev)
+    outs = [torch.empty(S, dm, dtype=torch.bfloat16, device=dev) for _ in range(min(L, 2))]
+    out = outs[0]
     torch.cuda.synchronize()
 
-    def step(sy, bs, ev=None):
-        if ev:
-            ev[0].record()
-        fo.project_q(x, params.w_q, params.q_norm, sy, "dispatch", out=q, fill=None, check=False)
-        if ev:
-            ev[1].record()
-        fo.sparse_attention(q, k, v, sy, cache, None, args.elapsed, args.interval, args.order,
-                            mode="bias", out=o, fill=None, check=False)
-        if ev:
-            ev[2].record()
-        fo.project_out_dispatch(o, params.w_out, sy, bs, args.elapsed, args.interval, args.order,
-                                out=out, check=False)
-        if group is not None:
-            dist.all_reduce(out, group=group)
-        if ev:
-            ev[3].record()
+    def phase_fns(dense, li, xin, lo):
+        ly = layers[li]
+        sy = dense_sym if dense else ly["sym"]
+        bs = ly["bias_dense"] if dense else ly["bias"]
+        return [lambda: fo.project_q(xin, ly["params"].w_q, ly["params"].q_norm, sy, "dispatch",
+                                     out=q, fill=None, check=False),
+                lambda: fo.sparse_attention(q, ly["k"], ly["v"], sy, ly["cache"], None,
+                                            args.elapsed, args.interval, args.order, mode="bias",
+                                            out=o, fill=None, check=False),
+                lambda: fo.project_out_dispatch(o, ly["params"].w_out, sy, bs, args.elapsed,
+                                                args.interval, args.order, out=lo, check=False)]
 
-    def timed(sy, bs, steps, warm, clocks=None):
+    graphs = {}
+
+    def phase_graphs(dense):
+        """each layer's three operators as CUDA graphs (the engine replays its
+        dispatch chains the same way, engine.py), captured once"""
+        if dense not in graphs:
+            cs = torch.cuda.Stream(device=dev)
+            cs.wait_stream(torch.cuda.current_stream())
+            gl, xin = [], x
+            with torch.cuda.stream(cs):
+                for li in range(L):
+                    lo = outs[li % len(outs)]
+                    gs = []
+                    for fn in phase_fns(dense, li, xin, lo):
+                        fn()  # first use outside capture (host-side tables, plans)
+                        gr = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(gr, stream=cs):
+                            fn()
+                        gs.append(gr)
+                    gl.append(gs)
+                    xin = lo
+            torch.cuda.current_stream().wait_stream(cs)
+            torch.cuda.synchronize()
+            graphs[dense] = gl
+        return graphs[dense]
+
+    def step(dense, ev=None):
+        """one dispatch step through the stack; ev: per layer, 4 events"""
+        gl = None if args.eager else phase_graphs(dense)
+        xin = x
+        for li in range(L):
+            e = ev[li] if ev else None
+            lo = outs[li % len(outs)]
+            fns = phase_fns(dense, li, xin, lo) if gl is None else [g.replay for g in gl[li]]
+            for k_ph in range(3):
+                if e:
+                    e[k_ph].record()
+                fns[k_ph]()
+            if group is not None:
+                dist.all_reduce(lo, group=group)
+            if e:
+                e[3].record()
+            xin = lo
+
+    def timed(dense, steps, warm, clocks=None):
         for _ in range(warm):
-            step(sy, bs)
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+            step(dense)
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(L)]
+               for _ in range(steps)]
         if group is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -326,14 +397,17 @@ def run_b200(args, cfg, rank, world):
             end = torch.cuda.Event(enable_timing=True)
             start.record()
             for s in range(steps):
-                step(sy, bs, evs[s])
+                step(dense, evs[s])
             end.record()
             torch.cuda.synchronize()
-        launches = _lib.launch_count()
+        launches = _lib.launch_count() if args.eager else launches_per_step * steps
         if group is not None:
             dist.barrier()
         total = start.elapsed_time(end)
-        parts = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])]
+        # per-phase ms per step, summed over the layers
+        parts = np.array([[sum(e[li][0].elapsed_time(e[li][1]) for li in range(L)),
+                           sum(e[li][1].elapsed_time(e[li][2]) for li in range(L)),
+                           sum(e[li][2].elapsed_time(e[li][3]) for li in range(L))]
                           for e in evs]).mean(axis=0)
         total_t = torch.tensor([total], device=dev)
         if group is not None:
@@ -341,21 +415,32 @@ def run_b200(args, cfg, rank, world):
         return total_t.item() / steps, parts, launches
 
     # check once that the contract holds (errors are latched, not raised, while timing)
-    step(sym, bias)
+    step(False)
     fo._runtime.Status.default().check("bench warm-up")
+    # kernels per step, counted on one eager step after the warm-up (graph replays
+    # launch the same kernels)
+    torch.cuda.synchronize()
+    _lib.reset_launch_count()
+    for fn_l in range(L):
+        for fn in phase_fns(False, fn_l, x if fn_l == 0 else outs[(fn_l - 1) % len(outs)],
+                            outs[fn_l % len(outs)]):
+            fn()
+    launches_per_step = _lib.launch_count()
+    torch.cuda.synchronize()
+
     clocks = Clocks(dev.index) if rank == 0 else None
-    ms, parts, launches = timed(sym, bias, args.steps, args.warmup, clocks)
+    ms, parts, launches = timed(False, args.steps, args.warmup, clocks)
     fo._runtime.Status.default().check("bench timed region")
     res = {"ms": ms, "parts": parts, "launches": launches}
     if not args.no_dense:
-        dms, dparts, _ = timed(dense_sym, bias_dense, max(3, args.steps // 2), 2)
+        dms, dparts, _ = timed(True, max(3, args.steps // 2), 2)
         res.update(dense_ms=dms, dense_parts=dparts)
 
     # e2e through the public API with host buffers: every step copies its x in
     # (pinned H2D) and its out back (D2H); pipeline.HostStepper overlaps step k's
     # compute with step k+1's input copy and step k-1's output copy
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and L == 1:
         state = fo.LayerState(params=params, cache=cache, symbols=sym, bias=bias)
         stepper = fo.HostStepper(state, S, dm, device=dev, group=group)
         x_host = [x.cpu().pin_memory() for _ in range(2)]
@@ -388,22 +473,23 @@ def run_b200(args, cfg, rank, world):
         return
     # ---------------- roofline of the dominant kernel (sparse attention)
     burst, sustained, hbm, src = peaks()
-    computed = int(sum(skip_bits[h][cache_bits[h]].sum() for h in heads))
-    attn_flops = 4.0 * T * T * T * computed
+    computed = sum(int(sum(ly["sb"][h][ly["cb"][h]].sum() for h in heads)) for ly in layers)
+    active = sum(int(ly["cb"][heads].sum()) for ly in layers)
+    attn_flops = 4.0 * T * T * T * computed / L  # per launch (one per layer)
     # Q of active tiles, K and V of every (head, block), O of active tiles (bf16)
-    attn_bytes = 2.0 * T * T * (2 * int(cache_bits[heads].sum()) + 2 * Hl * t)
-    ach = attn_flops / (parts[1] * 1e-3) / 1e12
+    attn_bytes = 2.0 * T * T * (2 * active / L + 2 * Hl * t)
+    ach = attn_flops * L / (parts[1] * 1e-3) / 1e12
     kname = ("sparse_attention_kernel" if os.environ.get("FO_ATTN_IMPL") == "v1"
              else "sparse_attention_cs_kernel")
     traffic, traffic_src = ncu_traffic(kname, args)
-    q_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
-    o_flops = 2.0 * dm * T * T * int(cache_bits[heads].sum())
+    q_flops = 2.0 * dm * T * T * active
+    o_flops = 2.0 * dm * T * T * active
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (N(0,1) activations, reference-init weights, random 8-bit symbols)",
-        "config": config_json(args, cfg, world, cache_bits, skip_bits),
+        "config": config_json(args, cfg, world, layers),
         "breakdown_ms": {"gemm_q": round(parts[0], 4), "attention": round(parts[1], 4),
                          "gemm_o_dispatch": round(parts[2], 4)},
         "effective_tflops": {"gemm_q": round(q_flops / parts[0] / 1e9, 1),
@@ -422,8 +508,8 @@ def run_b200(args, cfg, rank, world):
     }
     if "dense_ms" in res:
         dp = res["dense_parts"]
-        s_attn = 1 - computed / (Hl * t * t)
-        s_rows = 1 - int(cache_bits[heads].sum()) / (Hl * t)
+        s_attn = 1 - computed / (L * Hl * t * t)
+        s_rows = 1 - active / (L * Hl * t)
         ideal = {"attention": 1 / (1 - s_attn), "gemm_q": 1 / (1 - s_rows),
                  "gemm_o_dispatch": 1 / (1 - s_rows)}
         sp = {"gemm_q": dp[0] / parts[0], "attention": dp[1] / parts[1],
@@ -436,16 +522,19 @@ def run_b200(args, cfg, rank, world):
         line["frac_sparsity_scaled_roofline"] = {k2: round(sp[k2] / ideal[k2], 3) for k2 in sp}
         n_int = args.interval
         line["gemm_o_amortized_ideal"] = round(n_int / (1 + (n_int - 1) * (1 - s_rows)), 3)
-        dense_attn_tflops = 4.0 * T * T * T * Hl * t * t / (dp[1] * 1e-3) / 1e12
+        dense_attn_tflops = 4.0 * T * T * T * L * Hl * t * t / (dp[1] * 1e-3) / 1e12
         line["dense_attention_tflops"] = round(dense_attn_tflops, 1)
     if clocks is not None:
         line["clocks"] = clocks.summary()
     if e2e is not None:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu:
-        cms, sample, cparts, L = cpu_baseline(args, cfg, cache_bits, skip_bits)
+        cms, sample, cparts, CL = cpu_baseline(args, cfg, cache_bits, skip_bits)
+        if L > 1:
+            cms, cparts = cms * L, {k2: v2 * L for k2, v2 in cparts.items()}
+            sample += f"; layer 0 sampled, x {L} layers of the stack"
         line["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "cores": cpu_threads(),
-                                "kind": L.kind, "sample": sample,
+                                "kind": CL.kind, "sample": sample,
                                 "breakdown_ms": {k2: round(v2, 1) for k2, v2 in cparts.items()}}
     print(json.dumps(line), flush=True)
 

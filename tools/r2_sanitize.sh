@@ -1,0 +1,22 @@
+# compute-sanitizer memcheck / racecheck / synccheck on the small parity shapes:
+# the smoke step (codec, GEMM-Q, sparse attention, GEMM-O update + dispatch) and
+# a small engine run (policy, update-step attention with the cache push, graphs)
+mkdir -p gpurun_out/sanitize
+S=/usr/local/cuda/bin/compute-sanitizer
+cat > /tmp/san_engine.py <<'PY'
+import numpy as np, torch
+import paper_2509_25401_b200 as fo
+from paper_2509_25401_b200.engine import EngineConfig, run
+cfg = EngineConfig(n_text=128, n_vision=384, d_model=256, heads=2, tau_q=0.3, tau_kv=0.4,
+                   interval_n=3, order_d=1, steps=4, layers=1, seed=3)
+r = run(cfg, graphs=False)
+print("engine ok", r.report.sparsity)
+PY
+for tool in memcheck racecheck synccheck; do
+  for prog in "python -c 'import __graft_entry__ as g; g.smoke()'" "python /tmp/san_engine.py"; do
+    tag=$(echo "$prog" | grep -q smoke && echo smoke || echo engine)
+    echo "== $tool $tag"
+    timeout 1500 bash -c "$S --tool $tool --print-limit 20 --error-exitcode 9 $prog" > gpurun_out/sanitize/${tool}_${tag}.log 2>&1
+    echo "rc=$?"; tail -4 gpurun_out/sanitize/${tool}_${tag}.log
+  done
+done
