@@ -22,6 +22,9 @@
 
 // pairs (of every 8) whose exp2 runs as the FMA-pipe polynomial; with two
 // softmax warps per SMSP the MUFU is the tighter pipe, so more go to the FMA
+#ifndef FO_CS_ODONE_ALL
+#define FO_CS_ODONE_ALL 0  // 1: await every o_done phase (synccheck-clean, ~2% slower)
+#endif
 #ifndef FO_CS_POLY_OF_8
 #define FO_CS_POLY_OF_8 3
 #endif
@@ -358,8 +361,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
               mma_bf16_ts(tbase + TM_L, a_t + k * 8, ones_desc, idesc_l, (j > 0 || k > 0));
 #endif
             tc_commit(&bars->v_empty[vst]);
-            tc_commit(&bars->o_done);
-            if (j == n - 1) tc_commit(&bars->o_last);
+            // o_done: PV_j complete, awaited by softmax step j + 1 of this item;
+            // the item's last PV signals o_last (the epilogue) instead
+            if (j + 1 < n) tc_commit(&bars->o_done);
+            else tc_commit(&bars->o_last);
           }
           __syncwarp();
           if (++vst == VST) {
@@ -509,9 +514,16 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tmem_st16(sa + half * 16, pk);
 #endif
         tmem_st_wait();
+#if FO_CS_ODONE_ALL
+        // every o_done phase is awaited (PV_{j-1} has long finished by the time
+        // P_j is stored, so this costs nothing) and no phase goes unobserved
+        if (j > 0) mbar_wait_small(&bars->o_done, (o_base + j - 1) & 1, p.status);
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+#else
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // PV_{j-1} must be complete before O can be rescaled for P_j (see fo_attention.cu)
           mbar_wait_small(&bars->o_done, (o_base + j - 1) & 1, p.status);
+#endif
           tc_fence_after();
           const uint32_t oa = tbase + lane_off + TM_O + col0;
 #pragma unroll 1
@@ -552,7 +564,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         ++n_it;
       }
 #endif
-      o_base += n;
+      o_base += n - 1;  // o_done phases of this item
       tc_fence_after();
       float l_row;
       if (FO_CS_TC_ROWSUM) {
