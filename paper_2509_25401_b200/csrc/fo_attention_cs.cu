@@ -22,6 +22,9 @@
 
 // pairs (of every 8) whose exp2 runs as the FMA-pipe polynomial; with two
 // softmax warps per SMSP the MUFU is the tighter pipe, so more go to the FMA
+#ifndef FO_CS_VPROD
+#define FO_CS_VPROD 0  // 1: V tiles loaded by their own producer warp (warp 3)
+#endif
 #ifndef FO_CS_ODONE_ALL
 #define FO_CS_ODONE_ALL 0  // 1: await every o_done phase (synccheck-clean, ~2% slower)
 #endif
@@ -72,15 +75,28 @@ static_assert(SPLIT == 2 || SPLIT == 4, "column split of 2 or 4 warps per lane q
 static_assert(SPLIT == 2 || FO_CS_TC_ROWSUM, "a 4-way split needs the row sums in TMEM");
 constexpr int SOFTMAX_THREADS = 128 * SPLIT;
 constexpr int NTHREADS = 128 + SOFTMAX_THREADS;
-constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = 256;
+// S buffers in TMEM: QK(j + SBUF - 1) is issued while P(j) is produced. Two
+// buffers leave one tile of slack between a softmax step and the S it needs
+// next (S(j) waits on PV(j-2) + QK(j)); three need the row sums in registers
+// (O 128 + 3 x 128 S columns = all 512)
+#ifndef FO_CS_SBUF
+#define FO_CS_SBUF 2
+#endif
+constexpr int SBUF = FO_CS_SBUF;
+static_assert(SBUF == 2 || (SBUF == 3 && !FO_CS_TC_ROWSUM), "three S buffers need register row sums");
+constexpr uint32_t TM_O = 0, TM_L = 128, TM_S0 = SBUF == 3 ? 128 : 256;
 constexpr int ONES_BYTES = 2048;  // 16 rows x 128 B of bf16 1.0 (B operand of the row-sum MMA)
 
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[KST], k_empty[KST];
   uint64_t v_full[VST], v_empty[VST];
-  uint64_t s_full[2];
-  uint64_t p_full, o_done, o_last, o_free;
+  uint64_t s_full[SBUF];
+  // p_full[b]: P of the tiles using S buffer b stored (one phase per use). One
+  // barrier per buffer: a softmax step may finish P(j + 1) before the MMA warp,
+  // busy issuing QK(j + SBUF - 1), has observed P(j)
+  uint64_t p_full[SBUF];
+  uint64_t o_done, o_last, o_free;
   uint32_t tmem_base;
   float xmax[2][SPLIT][128];  // [tile parity][column group][row]: partial row maxima
   float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
@@ -170,9 +186,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       mbar_init(&bars->v_full[s], 1);
       mbar_init(&bars->v_empty[s], 1);
     }
-    mbar_init(&bars->s_full[0], 1);
-    mbar_init(&bars->s_full[1], 1);
-    mbar_init(&bars->p_full, SOFTMAX_THREADS / 32);  // one arrival per softmax warp
+    for (int b = 0; b < SBUF; ++b) mbar_init(&bars->s_full[b], 1);
+    for (int b = 0; b < SBUF; ++b)
+      mbar_init(&bars->p_full[b], SOFTMAX_THREADS / 32);  // one arrival per softmax warp
     mbar_init(&bars->o_done, 1);
     mbar_init(&bars->o_last, 1);
     mbar_init(&bars->o_free, SOFTMAX_THREADS);
@@ -255,6 +271,43 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             kst = 0;
             kph ^= 1;
           }
+          if (!FO_CS_VPROD) {
+            mbar_wait_small(&bars->v_empty[vst], vph ^ 1, p.status);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
+              uint8_t* dv = sV + vst * V_STAGE_BYTES;
+              tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
+              tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
+            }
+            __syncwarp();
+            if (++vst == VST) {
+              vst = 0;
+              vph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (FO_CS_VPROD && warp == 3) {
+    // ------------------------------------------------------------ V producer: walks the
+    // same item / key-block sequence as the K producer, so a K load never queues
+    // behind a V load waiting for its stage (QK runs ahead of PV)
+    int vst = 0, vph = 0;
+    ItemCursor sched_cur(p.sched, p.items, n_waves);
+    for (int k = 0; k < n_waves; ++k) {
+      int w;
+      int2 it;
+      if (!sched_cur.next(k, w, it)) break;
+      const int h = it.x >> 20, i = it.x & 0xFFFFF;
+      const uint8_t* sym = p.s_s + h * head_sym;
+      for (int base = 0; base < p.t_kv; base += 32) {
+        const int j = base + lane;
+        const uint32_t bit =
+            (j < p.t_kv) && (p.dense || decode_reduction(sym, p.row_stride, i, j, p.pool_n));
+        uint32_t m = __ballot_sync(0xffffffffu, bit);
+        while (m) {
+          const int jj = base + __ffs(m) - 1;
+          m &= m - 1;
           mbar_wait_small(&bars->v_empty[vst], vph ^ 1, p.status);
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
@@ -288,7 +341,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       auto issue_qk = [&]() {
         mbar_wait_small(&bars->k_full[kst], kph, p.status);
         tc_fence_after();
-        const uint32_t sb = qk_cnt & 1;
+        const uint32_t sb = qk_cnt % SBUF;
         const uint32_t d = tbase + TM_S0 + sb * 128;
         const uint64_t kdesc = kdesc0 + (uint64_t)((kst * TILE_BYTES) >> 4);
         if (elect_one()) {
@@ -325,29 +378,29 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (lane == 0 && k > 0) g_cs_timing[12 * blockIdx.x + 9] += global_ns() - t_pvl;
 #endif
         tc_fence_after();
-        issue_qk();
+        // QK runs SBUF - 1 tiles ahead of PV; Q is released after the item's last QK
+        const int la = n < SBUF - 1 ? n : SBUF - 1;
+        for (int a = 0; a < la; ++a) issue_qk();
 #ifdef FO_CS_TIMING
         if (k > 0) {
           const unsigned long long t0 = global_ns();
-          const uint32_t c = qk_cnt - 1;
-          while (!mbar_try_wait(&bars->s_full[c & 1], (c >> 1) & 1)) {
+          const uint32_t c = qk_cnt - la;
+          while (!mbar_try_wait(&bars->s_full[c % SBUF], (c / SBUF) & 1)) {
           }
           if (lane == 0) g_cs_timing[12 * blockIdx.x + 11] += global_ns() - t0;
         }
 #endif
-        if (n == 1) commit_q_empty();
+        if (la == n) commit_q_empty();
         for (int j = 0; j < n; ++j) {
-          if (j + 1 < n) {
+          if (j + la < n) {
             issue_qk();
-#ifdef FO_CS_TIMING
-#endif
-            if (j + 2 == n) commit_q_empty();
+            if (j + la + 1 == n) commit_q_empty();
           }
-          mbar_wait_small(&bars->p_full, pv_cnt & 1, p.status);
+          mbar_wait_small(&bars->p_full[pv_cnt % SBUF], (pv_cnt / SBUF) & 1, p.status);
           if (j == 0 && qi > 0) mbar_wait_small(&bars->o_free, (qi - 1) & 1, p.status);
           mbar_wait_small(&bars->v_full[vst], vph, p.status);
           tc_fence_after();
-          const uint32_t a_t = tbase + TM_S0 + (pv_cnt & 1) * 128;
+          const uint32_t a_t = tbase + TM_S0 + (pv_cnt % SBUF) * 128;
           const uint64_t vdesc = vdesc0 + (uint64_t)((vst * V_STAGE_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
@@ -419,11 +472,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       float m_run = -INFINITY;
       float2 l2 = make_float2(0.f, 0.f);
       for (int j = 0; j < n; ++j) {
-        const uint32_t sb = qk_seen & 1;
+        const uint32_t sb = qk_seen % SBUF;
 #ifdef FO_CS_TIMING
         if (tmr && j == 0 && t_mark) g_cs_timing[12 * blockIdx.x + 10] += global_ns() - t_mark;
 #endif
-        mbar_wait_small(&bars->s_full[sb], (qk_seen >> 1) & 1, p.status);
+        mbar_wait_small(&bars->s_full[sb], (qk_seen / SBUF) & 1, p.status);
 #ifdef FO_CS_TIMING
         if (tmr && j == 0 && t_mark) {
           const unsigned long long t = global_ns();
@@ -549,7 +602,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         }
         tc_fence_before();
         __syncwarp();  // every lane's P / O stores are complete (tcgen05.wait::st above)
-        if (lane == 0) mbar_arrive(&bars->p_full);
+        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
       }
       // ---------------- epilogue: this half of O / l -> bf16 -> HBM (+ cache push)
 #ifdef FO_CS_TIMING
