@@ -22,6 +22,13 @@
 
 // pairs (of every 8) whose exp2 runs as the FMA-pipe polynomial; with two
 // softmax warps per SMSP the MUFU is the tighter pipe, so more go to the FMA
+// 1: the epilogue stages each warp's 32 x 32 bf16 O chunk in shared memory and
+// TMA-stores it (4 L1 wavefronts per 16-B shared store instead of 32 per
+// uncoalesced 256-bit global store; the softmax warps' next shared-memory ops
+// no longer queue behind the stores)
+#ifndef FO_CS_TMA_OUT
+#define FO_CS_TMA_OUT 1
+#endif
 #ifndef FO_CS_VPROD
 #define FO_CS_VPROD 0  // 1: V tiles loaded by their own producer warp (warp 3)
 #endif
@@ -102,7 +109,10 @@ struct Bars {
   float xsum[2][128];     // [column half][row]: partial row sums at the epilogue
   int fc_tile;            // fused forecast: the tile the softmax warps take next
 };
-constexpr int SMEM_BYTES = SMEM_TILE_BYTES + ONES_BYTES + 1024 + (int)sizeof(Bars);
+// O staging: one 32-row x 32-column SW64 box (2 KB) per softmax warp
+constexpr int OSTAGE_BYTES = FO_CS_TMA_OUT ? SOFTMAX_THREADS / 32 * 2048 : 0;
+constexpr int SMEM_BYTES =
+    SMEM_TILE_BYTES + ONES_BYTES + OSTAGE_BYTES + 1024 + (int)sizeof(Bars);
 static_assert(SMEM_BYTES <= 232448, "column-split attention exceeds shared memory");
 }  // namespace attn_cs
 
@@ -155,7 +165,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
 __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     sparse_attention_cs_kernel(const __grid_constant__ CUtensorMap qm,
                                const __grid_constant__ CUtensorMap km,
-                               const __grid_constant__ CUtensorMap vm, const AttnParams p) {
+                               const __grid_constant__ CUtensorMap vm,
+                               const __grid_constant__ CUtensorMap om,  // out, 32 x 32 SW64
+                               const AttnParams p) {
   using namespace attn_cs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -164,7 +176,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   uint8_t* sK = smem + TILE_BYTES;
   uint8_t* sV = smem + TILE_BYTES * (1 + KST);
   uint8_t* sOnes = smem + SMEM_TILE_BYTES;  // 1024-aligned
-  Bars* bars = reinterpret_cast<Bars*>(sOnes + ONES_BYTES);
+  uint8_t* sOst = sOnes + ONES_BYTES;       // 1024-aligned (ONES_BYTES = 2 KB)
+  Bars* bars = reinterpret_cast<Bars*>(sOst + OSTAGE_BYTES);
   for (int e = threadIdx.x; e < ONES_BYTES / 4; e += blockDim.x)
     reinterpret_cast<uint32_t*>(sOnes)[e] = 0x3F803F80u;  // bf16 1.0 pairs
   if (FO_CS_ONESCOL)  // the ones strip behind each V stage (every byte 1.0, so swizzle-free)
@@ -652,6 +665,13 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
       }
       const uint32_t oa = tbase + lane_off + TM_O + col0;
+#if FO_CS_TMA_OUT
+      // this warp's staging box: rows q4*32.., its columns; chunk q of row r at
+      // q ^ ((r >> 1) & 3) (SW64, conflict-free for 8 consecutive rows)
+      const int wslot = warp - 4;
+      const uint32_t ost = smem_u32(sOst) + wslot * 2048 + lane * 64;
+      const int osw = (lane >> 1) & 3;
+#endif
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c) {
         uint32_t o[32];
@@ -661,8 +681,32 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         float of[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) of[k] = __uint_as_float(o[k]) * inv_l;
+#if FO_CS_TMA_OUT
+        {
+          uint4 pk4[4];
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            pk4[v4].x = pack_bf16x2(of[v4 * 8 + 0], of[v4 * 8 + 1]);
+            pk4[v4].y = pack_bf16x2(of[v4 * 8 + 2], of[v4 * 8 + 3]);
+            pk4[v4].z = pack_bf16x2(of[v4 * 8 + 4], of[v4 * 8 + 5]);
+            pk4[v4].w = pack_bf16x2(of[v4 * 8 + 6], of[v4 * 8 + 7]);
+          }
+          // the previous store from this box has read it (usually long done)
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) sts128(ost + ((v4 ^ osw) << 4), pk4[v4]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {  // rows past the end of the sequence are clipped by the TMA unit
+            tma_store_2d(&om, sOst + wslot * 2048, h * kTile + col0 + c * 32, i * kTile + q4 * 32);
+            bulk_commit();
+          }
+        }
+#endif
         if (row_ok) {
           const size_t off = (size_t)row * HD + (size_t)h * kTile + col0 + c * 32;
+#if !FO_CS_TMA_OUT
           uint4 pk4[4];
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
@@ -673,6 +717,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           }
           st_global_256(p.out + off, pk4[0], pk4[1]);
           st_global_256(p.out + off + 16, pk4[2], pk4[3]);
+#endif
           if (p.cache) {
             // backward-difference push: new[0]=o, new[d]=new[d-1]-old[d-1] for d<vn, else 0
             float cur[32];
@@ -734,6 +779,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       g_cs_timing[12 * blockIdx.x + 7] = n_it;
     }
 #endif
+#if FO_CS_TMA_OUT
+    if (lane == 0) bulk_wait<0>();  // this warp's O stores are complete
+    __syncwarp();
+#endif
     if (p.fc_cache)
       forecast_cached_tiles<SOFTMAX_THREADS>(p, threadIdx.x - 128, 8, &bars->fc_tile);
   }
@@ -756,7 +805,8 @@ extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigne
 #endif
 
 void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
-                         const AttnParams& p, int grid, cudaStream_t stream) {
+                         const CUtensorMap& om, const AttnParams& p, int grid,
+                         cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(sparse_attention_cs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -765,7 +815,7 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
   }
   note_launch();
   sparse_attention_cs_kernel<<<grid, attn_cs::NTHREADS, attn_cs::SMEM_BYTES, stream>>>(qm, km, vm,
-                                                                                     p);
+                                                                                     om, p);
 }
 
 }  // namespace fo

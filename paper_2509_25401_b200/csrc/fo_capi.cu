@@ -294,8 +294,12 @@ static int attention_common(const void* q, const void* k, const void* v, int seq
   fo_dbg_ptr = g_dbg;
 #endif
   if (!update_mode && !s_s) return fail(FO_ERR_PARAM, "s_s is NULL");
-  if (attention_impl() == 1)
-    launch_attention_cs(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
+  if (attention_impl() == 1) {
+    // O leaves through 32 x 32 SW64 TMA boxes (one per softmax warp and chunk)
+    CUtensorMap om;
+    if ((rc = make_map_ex(&om, out, seq, HD, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, "out"))) return rc;
+    launch_attention_cs(qm, km, vm, om, p, num_sms(), (cudaStream_t)stream);
+  }
   else
     launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);
   return check_launch("sparse_attention");

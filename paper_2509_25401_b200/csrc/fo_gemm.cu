@@ -32,6 +32,12 @@
 #ifndef FO_GO_EF_STORE
 #define FO_GO_EF_STORE FO_GO_EVICT_FIRST  // dispatch out stores evict-first
 #endif
+#ifndef FO_GU_EL_W
+#define FO_GU_EL_W 0  // update: W loads evict-last
+#endif
+#ifndef FO_GU_EF_STORE
+#define FO_GU_EF_STORE 1  // update: out / B_c stores evict-first
+#endif
 #ifndef FO_GO_EL_OPS
 #define FO_GO_EL_OPS 1  // dispatch o / W operand loads evict-last
 #endif
@@ -1027,11 +1033,21 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                 else
                   tma_load_2d_mc(st + rank * (A_BYTES / 2), &am, &bars->full[rg.s],
                                  h * 128 + kk * BK, j.i * BM + rank * (BM / 2), 0x3);
+#if FO_GU_EL_W
+                const uint64_t wpol = l2_evict_last_policy();
+                if (j.mine)
+                  tma_load_2d_hint(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
+                                   j.nb * TBN, wpol);
+                if (two)
+                  tma_load_2d_hint(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s],
+                                   h * 128 + kk * BK, j.nb * TBN + BN, wpol);
+#else
                 if (j.mine)
                   tma_load_2d(st + A_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK, j.nb * TBN);
                 if (two)
                   tma_load_2d(st + A_BYTES + B_BYTES, &wm, &bars->full[rg.s], h * 128 + kk * BK,
                               j.nb * TBN + BN);
+#endif
               }
               __syncwarp();
               rg.next();
@@ -1091,7 +1107,11 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const uint32_t ostage_u32 = smem_u32(ostage);
     const int sw = (r >> 1) & 3;  // SW64: 16-B chunk q of row r sits at q ^ ((r >> 1) & 3)
+#if FO_GU_EF_STORE
     const uint64_t pol = l2_evict_first_policy();
+#else
+    const uint64_t pol = l2_evict_normal_policy();
+#endif
     int uses[2] = {0, 0};
     int ob = 0;
     for (int w0 = next_valid(jstart); w0 < n_jobs;) {

@@ -182,7 +182,8 @@ void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtens
                       const AttnParams& p, int grid, cudaStream_t stream);
 // two softmax warpgroups splitting every tile's key columns (fo_attention_cs.cu)
 void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
-                         const AttnParams& p, int grid, cudaStream_t stream);
+                         const CUtensorMap& om, const AttnParams& p, int grid,
+                         cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // GEMMs

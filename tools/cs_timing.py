@@ -12,7 +12,8 @@ import paper_2509_25401_b200 as fo  # noqa: E402
 from paper_2509_25401_b200 import _lib  # noqa: E402
 from bench import random_masks  # noqa: E402
 
-T, S, H = 128, 33024, 24
+T, H = 128, 24
+S = int(sys.argv[3]) if len(sys.argv) > 3 else 33024
 t = S // T
 cached, skip = (float(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (0.25, 0.5)))
 dev = torch.device("cuda", 0)
