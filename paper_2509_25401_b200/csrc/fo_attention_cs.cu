@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     g_cs_timing[12 * blockIdx.x + 11] = 0;
   }
 #endif
+  pdl_release_and_wait();
   const int n_items = *p.n_items;
   const int n_waves = *p.n_waves;  // plan schedule: CTA b's k-th item is sched[k * grid + b]
   (void)n_items;
@@ -813,9 +814,18 @@ void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUt
                          attn_cs::SMEM_BYTES);
     configured = true;
   }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // FO_PDL (fo_common.cuh)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(attn_cs::NTHREADS);
+  cfg.dynamicSmemBytes = attn_cs::SMEM_BYTES;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = FO_PDL ? 1 : 0;
   note_launch();
-  sparse_attention_cs_kernel<<<grid, attn_cs::NTHREADS, attn_cs::SMEM_BYTES, stream>>>(qm, km, vm,
-                                                                                     om, p);
+  cudaLaunchKernelEx(&cfg, sparse_attention_cs_kernel, qm, km, vm, om, p);
 }
 
 }  // namespace fo

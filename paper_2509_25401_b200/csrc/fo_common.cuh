@@ -169,6 +169,21 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Programmatic dependent launch: every persistent kernel is launched with
+// programmatic stream serialization, releases its dependents at once and waits
+// for its predecessor's completion (and memory) after its shared-memory / TMEM
+// prologue, before its first global read. The next kernel's launch and
+// prologue then overlap this kernel's tail on the SMs it has left.
+#ifndef FO_PDL
+#define FO_PDL 1
+#endif
+__device__ __forceinline__ void pdl_release_and_wait() {
+#if FO_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

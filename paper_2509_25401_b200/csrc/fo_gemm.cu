@@ -178,11 +178,13 @@ template <typename Kernel, typename... Args>
 static void launch_pair_clusters_max(Kernel kernel, int smem, int* grid_cache, int max_ctas,
                                      cudaStream_t stream, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // FO_PDL (fo_common.cuh)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.blockDim = dim3(gemm::NTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -199,6 +201,7 @@ static void launch_pair_clusters_max(Kernel kernel, int smem, int* grid_cache, i
     *grid_cache = 2 * std::min(clusters, sms / 2);
   }
   cfg.gridDim = dim3(std::max(2, std::min(*grid_cache, max_ctas & ~1)));
+  cfg.numAttrs = FO_PDL ? 2 : 1;
   note_launch();
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
@@ -353,9 +356,6 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   float* nw_smem = reinterpret_cast<float*>(smem + Q2_STAGES * Q2_STAGE_BYTES + 1024);
   const int warp = warp_id(), lane = lane_id();
   const int rank = (int)cluster_ctarank();
-  if (p.norm_w)
-    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
-      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);   // the even CTA's producer arrives (tx from both CTAs)
@@ -375,6 +375,12 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+  pdl_release_and_wait();
+  if (p.norm_w) {
+    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
+      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
+    __syncthreads();
+  }
   const uint32_t tbase = bars->tmem_base;
   const int nph = p.H >> 1;            // full head pairs
   const int npj = nph + (p.H & 1);     // dense jobs per block pair (odd last head: N=128)
@@ -548,6 +554,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   __syncthreads();
   if (MC) cluster_sync();  // both CTAs' barriers exist before any multicast lands
   tc_fence_after();
+  pdl_release_and_wait();
   const uint32_t tbase = bars->tmem_base;
   const int nbn = (p.dm + TBN - 1) / TBN;
   // columns of n-tile nb (dispatch: the last tile is 128 wide when dm % 256 != 0)
@@ -968,6 +975,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+  pdl_release_and_wait();
   const uint32_t tbase = bars->tmem_base;
   const int nbn = (p.dm + TBN - 1) / TBN;
   auto tile_cols = [&](int nb) { return min(TBN, p.dm - nb * TBN); };
