@@ -387,6 +387,11 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   const int nbp = (p.t_q + 1) >> 1;    // block pairs
   const int n_cjobs = p.dense ? nbp * npj : *p.n_jobs;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // round rr of cluster cid takes job rr*ncl + cid, snaking (reversed on odd
+  // rounds): the plan lists the sparse jobs by cost class (N = 256, then
+  // N = 128 pairs, then single-block jobs), so clusters that drew a heavy job
+  // in one round draw a light one in the next
+  auto job_of = [&](int rr) { return rr * ncl + ((rr & 1) ? ncl - 1 - cid : cid); };
   const int nkb = p.dm / BK;
   // job -> this CTA's block i, head h and width (n256: heads h, h+1); false: no
   // block for this CTA (it loads zero rows past the end and skips its epilogue)
@@ -413,7 +418,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     // both CTAs load their own x rows and their half of B; the bytes of both
     // land on the even CTA's full barrier
     Ring<Q2_STAGES> rg;
-    for (int c = cid; c < n_cjobs; c += ncl) {
+    for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
+      const int c = job_of(rr);
+      if (c >= n_cjobs) continue;
       int i, h;
       bool n256;
       job(c, i, h, n256);  // a missing block loads zero rows (coordinates past the end)
@@ -440,7 +447,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const uint64_t desc0 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
     Ring<Q2_STAGES> rg;
     int t = 0;
-    for (int c = cid; c < n_cjobs; c += ncl, ++t) {
+    for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
+      const int c = job_of(rr);
+      if (c >= n_cjobs) continue;
       int i, h;
       bool n256;
       job(c, i, h, n256);
@@ -465,6 +474,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       }
       if (elect_one()) tc_commit_2sm_mc(&bars->tfull[acc], 0x3);
       __syncwarp();
+      ++t;
     }
   } else if (warp >= 4) {
     const int q4 = warp & 3;
@@ -472,7 +482,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const uint32_t nw_u32 = smem_u32(nw_smem);
     int t = 0;
-    for (int c = cid; c < n_cjobs; c += ncl, ++t) {
+    for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
+      const int c = job_of(rr);
+      if (c >= n_cjobs) continue;
       int i, h;
       bool n256;
       const bool mine = job(c, i, h, n256);
@@ -489,6 +501,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
                              release);
       else
         release();
+      ++t;
     }
   }
   tc_fence_before();

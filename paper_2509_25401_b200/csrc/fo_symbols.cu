@@ -431,14 +431,25 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     }
     __syncthreads();
     const int n2 = pv.counts[7];
-    int* bcnt = hist;  // [rows] jobs per first block (hist is free after pass 2)
-    for (int i = tid; i < rows; i += nt) bcnt[i] = 0;
+    // counting sort by (cost class, first block): N = 256 two-block jobs, then
+    // N = 128 two-block jobs, then single-block jobs, each by first block (jobs
+    // in flight share x tiles in L2; the kernel deals the classes out snaking)
+    const int avail = nseg * (cols + 2) + 3072;  // ints of plan_smem free after pass 2
+    const int ncls = 3 * rows <= avail ? 3 : 1;
+    auto key = [&](int2 code) {
+      const int i0 = code.x & 0xFFFF;
+      if (ncls == 1) return i0;
+      const int cls = (code.x >> 16) == 0 ? 2 : (((code.y >> 8) & 1) ? 0 : 1);
+      return cls * rows + i0;
+    };
+    int* bcnt = plan_smem;  // [ncls * rows] (free after pass 2)
+    for (int i = tid; i < ncls * rows; i += nt) bcnt[i] = 0;
     __syncthreads();
-    for (int e = tid; e < n2; e += nt) atomicAdd(&bcnt[tmp[e].x & 0xFFFF], 1);
+    for (int e = tid; e < n2; e += nt) atomicAdd(&bcnt[key(tmp[e])], 1);
     __syncthreads();
     if (tid == 0) {
       int run = 0;
-      for (int i = 0; i < rows; ++i) {
+      for (int i = 0; i < ncls * rows; ++i) {
         const int c = bcnt[i];
         bcnt[i] = run;
         run += c;
@@ -447,7 +458,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
     __syncthreads();
     for (int e = tid; e < n2; e += nt) {
       const int2 code = tmp[e];
-      pv.gq_jobs[atomicAdd(&bcnt[code.x & 0xFFFF], 1)] = code;
+      pv.gq_jobs[atomicAdd(&bcnt[key(code)], 1)] = code;
     }
   }
 }

@@ -62,7 +62,7 @@ def cache_masks(rng, heads, t, cached_ratio):
 def check_gq_jobs(plan, active):
     """Every active (block, head) tile is in exactly one GEMM-Q job, no cached
     tile is in any, N=256 jobs pair heads (2p, 2p+1) active together, and the
-    list is ordered by first block."""
+    list is ordered by cost class, then by first block."""
     jobs = plan.gq_jobs()
     H, t = active.shape
     seen = np.zeros((H, t), int)
@@ -76,7 +76,12 @@ def check_gq_jobs(plan, active):
             for hh in heads:
                 seen[hh, i] += 1
     assert np.array_equal(seen, active.astype(int))
-    assert np.all(np.diff(jobs[:, 0]) >= 0)
+    # ordered by cost class (N=256 pairs of blocks, N=128 pairs, single-block
+    # jobs), then by first block
+    cls = np.where(jobs[:, 1] < 0, 2, np.where(jobs[:, 3] > 0, 0, 1))
+    assert np.all(np.diff(cls) >= 0)
+    for c in range(3):
+        assert np.all(np.diff(jobs[cls == c, 0]) >= 0)
     return jobs
 
 
