@@ -212,3 +212,69 @@ def test_feature_cache_update_tile_sized():
         fc.update(3, 0, np.zeros((128, 128), np.float32))
     with pytest.raises(m.ShapeError):
         fc.update(0, 0, np.zeros((44, 128), np.float32))
+
+
+# ---------------------------------------------------------------------------
+# The reference's known-answer properties of the cache and the forecast
+# (test_attention.py:85-160, test_acceptance.py:235-253), on the
+# device update_entry / forecast / FeatureCache.
+# ---------------------------------------------------------------------------
+def test_forecast_affine_trajectories_exact():
+    m = fo()
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        a = rng.standard_normal((8, 16)).astype(np.float32)
+        b = (0.2 * rng.standard_normal((8, 16))).astype(np.float32)
+        n = int(rng.integers(2, 8))
+        f = lambda t: (a + t * b).astype(np.float32)  # noqa: E731
+        e = m.update_entry(m.update_entry(None, f(0), 1), f(n), 1)
+        for k in range(1, n):
+            got = m.forecast(e, k, n, 1)
+            assert np.abs(got - f(n + k)).max() / np.abs(f(n + k)).max() < 1e-5
+        const = m.update_entry(None, a, 0)  # order 0: exact reuse after one update
+        np.testing.assert_array_equal(m.forecast(const, 1, n, 0), a)
+
+
+def test_quadratic_second_difference_and_repeats():
+    m = fo()
+    rng = np.random.default_rng(5)
+    a, b, c = (rng.standard_normal((4, 8)).astype(np.float32) for _ in range(3))
+    f = lambda t: (a + t * b + t * t * c).astype(np.float32)  # noqa: E731
+    e = None
+    for t in (0, 1, 2):
+        e = m.update_entry(e, f(t), 2)
+    assert e.valid_orders == 3
+    np.testing.assert_allclose(e.diff_stack[2], 2 * c, atol=1e-5)
+    o = rng.standard_normal((4, 8)).astype(np.float32)
+    e2 = m.update_entry(m.update_entry(None, o, 1), o, 1)  # a repeated tile: zero difference
+    assert e2.valid_orders == 2 and not e2.diff_stack[1].any()
+
+
+def test_forecast_hand_coefficients_and_exact_linearity():
+    m = fo()
+    assert m.forecast_coefficients(2, 4, 2).tolist() == [1.0, 0.5]
+    s0 = np.full((2, 2), 4.0, np.float32)
+    s1 = np.full((2, 2), 2.0, np.float32)
+    e = m.update_entry(m.update_entry(None, s0 - s1, 1), s0, 1)
+    np.testing.assert_array_equal(e.diff_stack[0], s0)
+    np.testing.assert_array_equal(e.diff_stack[1], s1)
+    np.testing.assert_array_equal(m.forecast(e, 2, 4, 1), s0 + 0.5 * s1)
+    # coefficients 1, 1/2, 1/8 and small-integer stacks: every operation exact
+    rng = np.random.default_rng(9)
+    ints = lambda: rng.integers(-8, 9, (3, 4)).astype(np.float32)  # noqa: E731
+    s_a, s_b = [ints() for _ in range(3)], [ints() for _ in range(3)]
+    entry = lambda st: m.CacheEntry(diff_stack=np.stack(st), valid_orders=3)  # noqa: E731
+    lhs = m.forecast(entry([3.0 * x + 5.0 * y for x, y in zip(s_a, s_b)]), 2, 4, 2)
+    rhs = 3.0 * m.forecast(entry(s_a), 2, 4, 2) + 5.0 * m.forecast(entry(s_b), 2, 4, 2)
+    np.testing.assert_array_equal(lhs, rhs)
+
+
+def test_feature_cache_valid_order_counting():
+    """FeatureCache.update on the device counts valid orders as the reference
+    (test_attention.py:101-106): min(updates, order + 1)."""
+    m = fo()
+    cache = m.FeatureCache(1, 1, 2, seq=128)
+    rng = np.random.default_rng(6)
+    for u in range(1, 6):
+        cache.update(0, 0, rng.standard_normal((128, 128)).astype(np.float32))
+        assert cache.valid_orders(0, 0) == min(u, 3)

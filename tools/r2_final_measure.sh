@@ -18,3 +18,7 @@ timeout 600 python tools/gemm_time.py > gpurun_out/gemm_time_r02_$TAG.json 2>/de
 timeout 600 python tools/gemm_time.py --seq 4096 > gpurun_out/gemm_time4k_r02_$TAG.json 2>/dev/null
 timeout 1800 python tools/sweep.py --out gpurun_out/sweep_r02_$TAG.json > /dev/null 2> gpurun_out/sweep_r02_$TAG.err; echo "sweep rc=$?"
 ls -la gpurun_out/ | grep $TAG
+for c in c1 c2 c5; do
+  timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_r02_$TAG.json 2> /dev/null; echo "$c rc=$?"
+done
+timeout 600 python tools/external_check.py > gpurun_out/external_r02_$TAG.json 2>/dev/null; echo "external rc=$?"
