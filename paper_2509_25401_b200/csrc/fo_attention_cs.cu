@@ -134,10 +134,12 @@ struct ItemCursor {
   const int2* items;
   int n_waves, w1, w2;
   int2 it1;
-  __device__ ItemCursor(const int* s, const int2* its, int nw) : sched(s), items(its), n_waves(nw) {
-    w1 = nw > 0 ? s[blockIdx.x] : -1;
+  int slot, nslots;  // schedule column (CTA, or cluster in the CTA-pair kernel) and width
+  __device__ ItemCursor(const int* s, const int2* its, int nw, int sl, int ns)
+      : sched(s), items(its), n_waves(nw), slot(sl), nslots(ns) {
+    w1 = nw > 0 ? s[sl] : -1;
     it1 = w1 >= 0 ? its[w1] : make_int2(0, 0);
-    w2 = nw > 1 ? s[gridDim.x + blockIdx.x] : -1;
+    w2 = nw > 1 ? s[ns + sl] : -1;
   }
   // item k (call with k = 0, 1, ...): false at the end of the schedule
   __device__ __forceinline__ bool next(int k, int& w, int2& it) {
@@ -146,7 +148,7 @@ struct ItemCursor {
     if (w < 0) return false;
     w1 = w2;
     it1 = w2 >= 0 ? items[w2] : make_int2(0, 0);
-    w2 = k + 2 < n_waves ? sched[(k + 2) * gridDim.x + blockIdx.x] : -1;
+    w2 = k + 2 < n_waves ? sched[(k + 2) * nslots + slot] : -1;
     return true;
   }
   __device__ __forceinline__ int peek_w() const { return w1; }
@@ -162,6 +164,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 #endif
 
+// PAIR: 2-CTA clusters for pooled symbols (pool_n even). Query blocks 2c and
+// 2c+1 share one compressed skip row, so the CTAs of a cluster take them
+// together (item (h, 2c); a missing 2c+1 is a zero-filled block past the end)
+// and walk the same K/V sequence in lockstep: each CTA TMA-loads one 64-column
+// half of every K and V tile and multicasts it to both, halving the K/V reads
+// from L2. A stage is refilled once both CTAs' MMAs have released it.
+template <bool PAIR>
 __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     sparse_attention_cs_kernel(const __grid_constant__ CUtensorMap qm,
                                const __grid_constant__ CUtensorMap km,
@@ -187,17 +196,32 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
   const int warp = warp_id(), lane = lane_id();
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;  // this CTA's block: item block + rank
+  const int slot = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nslots = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  constexpr uint32_t kEmptyCount = PAIR ? 2 : 1;  // both CTAs' MMAs release a K/V stage
+  // one K or V tile (two 64-column SW128 halves) into a stage; in a pair each
+  // CTA loads its half and multicasts it (the full barrier of each CTA counts
+  // the bytes of both halves)
+  auto load_tile = [&](uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int h, int jj) {
+    if (PAIR) {
+      tma_load_2d_mc(dst + rank * HALF_BYTES, map, bar, h * kTile + rank * 64, jj * kTile, 0x3);
+    } else {
+      tma_load_2d(dst, map, bar, h * kTile, jj * kTile);
+      tma_load_2d(dst + HALF_BYTES, map, bar, h * kTile + 64, jj * kTile);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
     for (int s = 0; s < KST; ++s) {
       mbar_init(&bars->k_full[s], 1);
-      mbar_init(&bars->k_empty[s], 1);
+      mbar_init(&bars->k_empty[s], kEmptyCount);
     }
     for (int s = 0; s < VST; ++s) {
       mbar_init(&bars->v_full[s], 1);
-      mbar_init(&bars->v_empty[s], 1);
+      mbar_init(&bars->v_empty[s], kEmptyCount);
     }
     for (int b = 0; b < SBUF; ++b) mbar_init(&bars->s_full[b], 1);
     for (int b = 0; b < SBUF; ++b)
@@ -213,6 +237,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // both CTAs' barriers exist before any multicast lands
   tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
 #ifdef FO_CS_TIMING
@@ -237,12 +262,12 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     int kst = 0, kph = 0, vst = 0, vph = 0, qi = 0;
-    ItemCursor sched_cur(p.sched, p.items, n_waves);
+    ItemCursor sched_cur(p.sched, p.items, n_waves, slot, nslots);
     for (int k = 0; k < n_waves; ++k, ++qi) {
       int w;
       int2 it;
       if (!sched_cur.next(k, w, it)) break;
-      const int h = it.x >> 20, i = it.x & 0xFFFFF;
+      const int h = it.x >> 20, i = it.x & 0xFFFFF, ib = i + rank;
 #ifdef FO_CS_TIMING
       const unsigned long long tq0 = global_ns();
 #endif
@@ -252,15 +277,15 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #endif
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
-        tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, i * kTile);
-        tma_load_2d(sQ + HALF_BYTES, &qm, &bars->q_full, h * kTile + 64, i * kTile);
+        tma_load_2d(sQ, &qm, &bars->q_full, h * kTile, ib * kTile);
+        tma_load_2d(sQ + HALF_BYTES, &qm, &bars->q_full, h * kTile + 64, ib * kTile);
         // the next item's Q into L2 now: its load is only issued once this
         // item's last QK is done, and from HBM it would stall the next item's
         // first QK by ~1 us
         if (sched_cur.peek_w() >= 0) {
           const int2 itn = sched_cur.peek_item();
-          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile, (itn.x & 0xFFFFF) * kTile);
-          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile + 64, (itn.x & 0xFFFFF) * kTile);
+          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile, ((itn.x & 0xFFFFF) + rank) * kTile);
+          tma_prefetch_l2_2d(&qm, (itn.x >> 20) * kTile + 64, ((itn.x & 0xFFFFF) + rank) * kTile);
         }
       }
       __syncwarp();
@@ -277,8 +302,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->k_full[kst], TILE_BYTES);
             uint8_t* dk = sK + kst * TILE_BYTES;
-            tma_load_2d(dk, &km, &bars->k_full[kst], h * kTile, jj * kTile);
-            tma_load_2d(dk + HALF_BYTES, &km, &bars->k_full[kst], h * kTile + 64, jj * kTile);
+            load_tile(dk, &km, &bars->k_full[kst], h, jj);
           }
           __syncwarp();
           if (++kst == KST) {
@@ -290,8 +314,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             if (elect_one()) {
               mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
               uint8_t* dv = sV + vst * V_STAGE_BYTES;
-              tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
-              tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
+              load_tile(dv, &vm, &bars->v_full[vst], h, jj);
             }
             __syncwarp();
             if (++vst == VST) {
@@ -307,7 +330,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     // same item / key-block sequence as the K producer, so a K load never queues
     // behind a V load waiting for its stage (QK runs ahead of PV)
     int vst = 0, vph = 0;
-    ItemCursor sched_cur(p.sched, p.items, n_waves);
+    ItemCursor sched_cur(p.sched, p.items, n_waves, slot, nslots);
     for (int k = 0; k < n_waves; ++k) {
       int w;
       int2 it;
@@ -326,8 +349,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (elect_one()) {
             mbar_arrive_expect_tx(&bars->v_full[vst], TILE_BYTES);
             uint8_t* dv = sV + vst * V_STAGE_BYTES;
-            tma_load_2d(dv, &vm, &bars->v_full[vst], h * kTile, jj * kTile);
-            tma_load_2d(dv + HALF_BYTES, &vm, &bars->v_full[vst], h * kTile + 64, jj * kTile);
+            load_tile(dv, &vm, &bars->v_full[vst], h, jj);
           }
           __syncwarp();
           if (++vst == VST) {
@@ -364,7 +386,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             const uint64_t off = (uint64_t)((k >> 2) * (HALF_BYTES >> 4) + (k & 3) * 2);
             mma_bf16_ss(d, qdesc + off, kdesc + off, idesc_qk, k > 0);
           }
-          tc_commit(&bars->k_empty[kst]);
+          if (PAIR)
+            tc_commit_mc(&bars->k_empty[kst], 0x3);  // released in both CTAs' view
+          else
+            tc_commit(&bars->k_empty[kst]);
           tc_commit(&bars->s_full[sb]);
         }
         __syncwarp();
@@ -378,7 +403,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         if (elect_one()) tc_commit(&bars->q_empty);
         __syncwarp();
       };
-      ItemCursor sched_cur(p.sched, p.items, n_waves);
+      ItemCursor sched_cur(p.sched, p.items, n_waves, slot, nslots);
 #ifdef FO_CS_TIMING
       unsigned long long t_pvl = 0;
 #endif
@@ -427,7 +452,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
             for (int k = 0; k < 8; ++k)
               mma_bf16_ts(tbase + TM_L, a_t + k * 8, ones_desc, idesc_l, (j > 0 || k > 0));
 #endif
-            tc_commit(&bars->v_empty[vst]);
+            if (PAIR)
+              tc_commit_mc(&bars->v_empty[vst], 0x3);
+            else
+              tc_commit(&bars->v_empty[vst]);
             // o_done: PV_j complete, awaited by softmax step j + 1 of this item;
             // the item's last PV signals o_last (the epilogue) instead
             if (j + 1 < n) tc_commit(&bars->o_done);
@@ -461,7 +489,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t qk_seen = 0, o_base = 0;
     int qi = 0;
-    ItemCursor sched_cur(p.sched, p.items, n_waves);
+    ItemCursor sched_cur(p.sched, p.items, n_waves, slot, nslots);
     // the next item's record and cache counter are fetched before this item's
     // epilogue stores: a global load or atomic issued behind 8 uncoalesced
     // 16-B stores per thread waits for them to drain (~0.9 us per item)
@@ -647,7 +675,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         l_row = bars->xsum[0][r] + bars->xsum[1][r];
       }
       const float inv_l = 1.f / l_row;
-      const int row = i * kTile + r;
+      const int ib = i + rank;  // this CTA's query block (a pair's missing partner: ib == t_q)
+      const int row = ib * kTile + r;
       const bool row_ok = row < p.S;
       const int vn = min(valid_old + 1, p.order_d + 1);
       {
@@ -661,9 +690,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #ifdef FO_CS_TIMING
         atomicAdd(&g_cs_timing[12 * blockIdx.x + 3], (unsigned long long)n);
 #endif
-        if (p.pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
-                               static_cast<unsigned long long>(n));
-        if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + i] = vn;
+        if (p.pairs && ib < p.t_q)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
+                    static_cast<unsigned long long>(n));
+        if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + ib] = vn;
       }
       const uint32_t oa = tbase + lane_off + TM_O + col0;
 #if FO_CS_TMA_OUT
@@ -700,7 +730,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {  // rows past the end of the sequence are clipped by the TMA unit
-            tma_store_2d(&om, sOst + wslot * 2048, h * kTile + col0 + c * 32, i * kTile + q4 * 32);
+            tma_store_2d(&om, sOst + wslot * 2048, h * kTile + col0 + c * 32, ib * kTile + q4 * 32);
             bulk_commit();
           }
         }
@@ -789,6 +819,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal into it
 #ifdef FO_CS_TIMING
   if (threadIdx.x == 0) g_cs_timing[12 * blockIdx.x + 1] = global_ns();
 #endif
@@ -806,26 +837,40 @@ extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigne
 #endif
 
 void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
-                         const CUtensorMap& om, const AttnParams& p, int grid,
+                         const CUtensorMap& om, const AttnParams& p, int grid, bool pair,
                          cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(sparse_attention_cs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         attn_cs::SMEM_BYTES);
+    cudaFuncSetAttribute(sparse_attention_cs_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, attn_cs::SMEM_BYTES);
+    cudaFuncSetAttribute(sparse_attention_cs_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, attn_cs::SMEM_BYTES);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // FO_PDL (fo_common.cuh)
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3(grid);
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (FO_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // fo_common.cuh
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (pair) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
+  cfg.gridDim = dim3(pair ? grid & ~1 : grid);
   cfg.blockDim = dim3(attn_cs::NTHREADS);
   cfg.dynamicSmemBytes = attn_cs::SMEM_BYTES;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = FO_PDL ? 1 : 0;
+  cfg.numAttrs = na;
   note_launch();
-  cudaLaunchKernelEx(&cfg, sparse_attention_cs_kernel, qm, km, vm, om, p);
+  if (pair)
+    cudaLaunchKernelEx(&cfg, sparse_attention_cs_kernel<true>, qm, km, vm, om, p);
+  else
+    cudaLaunchKernelEx(&cfg, sparse_attention_cs_kernel<false>, qm, km, vm, om, p);
 }
 
 }  // namespace fo

@@ -228,8 +228,13 @@ int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int col
   }
   if (rows > 65535) return fail(FO_ERR_PARAM, "too many query blocks for the plan (%d)", rows);
   note_launch();
+  // CTA-pair attention for even pool_n (sparse): the schedule has one slot per cluster
+  // (the v1 kernel, FO_ATTN_IMPL=v1, runs one block per item)
+  const bool pair = attention_impl() == 1 && attention_pairs(pool_n, dense);
+  const int slots = pair ? num_sms() / 2 : num_sms();
   plan_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(s_c, s_s, heads, rows, cols, pool_n, dense,
-                                                       valid, order_d, num_sms(), pv, status);
+                                                       valid, order_d, slots, pair ? 1 : 0, pv,
+                                                       status);
   return check_launch("plan");
 }
 
@@ -298,7 +303,10 @@ static int attention_common(const void* q, const void* k, const void* v, int seq
     // O leaves through 32 x 32 SW64 TMA boxes (one per softmax warp and chunk)
     CUtensorMap om;
     if ((rc = make_map_ex(&om, out, seq, HD, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B, "out"))) return rc;
-    launch_attention_cs(qm, km, vm, om, p, num_sms(), (cudaStream_t)stream);
+    // pooled symbols (pool_n even, sparse): CTA pairs with K/V multicast; the
+    // plan was built with the matching pair items (fo_plan)
+    const bool pair = attention_pairs(pool_n, update_mode);
+    launch_attention_cs(qm, km, vm, om, p, num_sms(), pair, (cudaStream_t)stream);
   }
   else
     launch_attention(qm, km, vm, p, num_sms(), (cudaStream_t)stream);

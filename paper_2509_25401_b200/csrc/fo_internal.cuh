@@ -13,7 +13,8 @@ __host__ __device__ constexpr int ceil_div_d(int a, int b) { return (a + b - 1) 
 struct PlanView {
   int* counts;                // [0] attention items, [1] GEMM-Q (= active) tiles,
                               // [2] fused-forecast tile cursor, [3] CTAs done (both self-resetting),
-                              // [4], [5] unused,
+                              // [4] 1: items cover CTA pairs of query blocks (pool_n even),
+                              // [5] attention schedule slots per wave (CTAs or clusters),
                               // [6] attention waves of the balanced schedule,
                               // [7] GEMM-Q jobs (gq_jobs)
   int2* items;                // [H*rows] attention work: x = (h<<20)|i, y = #KV blocks; sorted desc
@@ -75,7 +76,13 @@ __global__ void decode_symbols_kernel(const uint8_t* s_c, const uint8_t* s_s, in
                                       int cols, int pool_n, uint8_t* active, uint8_t* pair_bits);
 __global__ void plan_kernel(const uint8_t* s_c, const uint8_t* s_s, int H, int rows, int cols,
                             int pool_n, int dense, const int32_t* valid, int order_d, int ctas,
-                            PlanView pv, uint32_t* status);
+                            int pair_items, PlanView pv, uint32_t* status);
+// CTA-pair attention with K/V multicast: sparse plans over even pool_n (their
+// query blocks 2c, 2c+1 share one compressed skip row)
+#ifndef FO_ATTN_PAIR
+#define FO_ATTN_PAIR 1
+#endif
+inline bool attention_pairs(int pool_n, int dense) { return FO_ATTN_PAIR && !dense && pool_n % 2 == 0; }
 __global__ void compare_active_kernel(const uint8_t* s_c_a, const uint8_t* s_c_b, int H, int rows,
                                       int pool_n, uint32_t* status);
 
@@ -182,7 +189,7 @@ void launch_attention(const CUtensorMap& qm, const CUtensorMap& km, const CUtens
                       const AttnParams& p, int grid, cudaStream_t stream);
 // two softmax warpgroups splitting every tile's key columns (fo_attention_cs.cu)
 void launch_attention_cs(const CUtensorMap& qm, const CUtensorMap& km, const CUtensorMap& vm,
-                         const CUtensorMap& om, const AttnParams& p, int grid,
+                         const CUtensorMap& om, const AttnParams& p, int grid, bool pair,
                          cudaStream_t stream);
 
 // ---------------------------------------------------------------------------

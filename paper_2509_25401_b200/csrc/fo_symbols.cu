@@ -100,7 +100,7 @@ __global__ void decode_symbols_kernel(const uint8_t* __restrict__ s_c, const uin
 __global__ void __launch_bounds__(1024, 1)
 plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, int H, int rows,
             int cols, int pool_n, int dense, const int32_t* __restrict__ valid, int order_d,
-            int ctas, PlanView pv, uint32_t* status) {
+            int ctas, int pair_items, PlanView pv, uint32_t* status) {
   // Attention items are ordered head-major, longest rows first within a head:
   // CTAs stride through the list together, so the K/V of the ~1-2 heads in
   // flight stay L2-resident while per-CTA work stays balanced.
@@ -114,6 +114,11 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   const int tid = threadIdx.x, nt = blockDim.x;
   const int total = H * rows;
   auto seg = [&](int h) { return nseg == 1 ? 0 : h; };
+  // CTA-pair attention (pool_n even, sparse): query blocks 2c and 2c+1 share one
+  // compressed skip row, so one item (h, 2c) covers both (one per CTA of a
+  // cluster, K/V multicast); the schedule then has `ctas` = clusters slots
+  const bool pair = pair_items != 0;
+  auto scheduled = [&](int i) { return !pair || (i & 1) == 0; };
 
   for (int c = tid; c < nseg * (cols + 2); c += nt) hist[c] = 0;
   for (int h = tid; h < 64; h += nt) s_pairs[h] = 0;
@@ -192,7 +197,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
         // active query block with every key block skipped (pyref.py:43-46)
         raise_status(status, ST_CONSISTENCY);
       } else {
-        atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
+        if (scheduled(i)) atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
         atomicAdd(&s_pairs[h], (unsigned int)cnt);
       }
     } else if (valid && valid[(size_t)h * rows + i] < 1) {
@@ -245,7 +250,7 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
   // pass 2: scatter attention items (sorted by KV count, descending)
   for (int idx = tid; idx < total; idx += nt) {
     const int cnt = kvc[idx];  // -1 cached, 0 empty (flagged above)
-    if (cnt > 0) {
+    if (cnt > 0 && scheduled(idx % rows)) {
       const int h = idx / rows, i = idx % rows;
       int pos = atomicAdd(&hist[seg(h) * (cols + 2) + cnt], 1);
       pv.items[pos] = make_int2((h << 20) | i, cnt);
@@ -336,7 +341,11 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
       if (tid < min(P, n_items - nbase)) wave_len[tid] = next_len;
       __syncthreads();
     }
-    if (tid == 0) pv.counts[6] = n_waves;
+    if (tid == 0) {
+      pv.counts[6] = n_waves;
+      pv.counts[4] = pair ? 1 : 0;  // attention items cover CTA pairs (2c, 2c+1)
+      pv.counts[5] = P;             // schedule slots per wave
+    }
   }
   __syncthreads();
   // pass 3: GEMM-Q tile list in (block, head) order: compaction via block scan
@@ -403,8 +412,6 @@ plan_kernel(const uint8_t* __restrict__ s_c, const uint8_t* __restrict__ s_s, in
         run += c;
       }
       pv.counts[7] = run;
-      pv.counts[4] = 0;
-      pv.counts[5] = 0;
     }
     __syncthreads();
     int2* tmp = pv.gq_jobs + gq_jobs_cap(H, rows);  // unsorted jobs

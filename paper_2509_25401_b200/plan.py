@@ -60,6 +60,11 @@ class Plan:
         it = self._view(1, torch.int32, 2 * self.heads * self.rows).view(-1, 2)[:n].cpu().numpy()
         return np.stack([it[:, 0] >> 20, it[:, 0] & 0xFFFFF, it[:, 1]], axis=1)
 
+    def pair_items(self):
+        """True when each attention item (h, i) covers query blocks i and i + 1
+        on the two CTAs of a cluster (pool_n even: they share a skip row)."""
+        return bool(int(self.counts()[4]))
+
     def gq_items(self):
         n = int(self.counts()[1])
         it = self._view(2, torch.int32, self.heads * self.rows)[:n].cpu().numpy()
@@ -75,11 +80,12 @@ class Plan:
         return self._view(5, torch.int64, self.heads).cpu().numpy()
 
     def schedule(self):
-        """Attention schedule: int32 [n_waves, num_sms], the item index (into
-        items()) each CTA runs in each wave, -1 for none."""
+        """Attention schedule: int32 [n_waves, slots], the item index (into
+        items()) each CTA (each CTA pair when pair_items()) runs in each wave,
+        -1 for none."""
         lib = _lib.load()
         off = int(lib.fo_plan_schedule_offset(self.heads, self.rows))
-        n_waves, ctas = int(self.counts()[6]), int(lib.fo_num_sms())
+        n_waves, ctas = int(self.counts()[6]), int(self.counts()[5])
         n = n_waves * ctas
         return self.ws[off:off + 4 * n].view(torch.int32).cpu().numpy().reshape(n_waves, ctas)
 
