@@ -38,6 +38,10 @@
 #ifndef FO_CS_POLY_OF_8
 #define FO_CS_POLY_OF_8 3
 #endif
+// finer split: pairs (of every 16) on the polynomial; default 2 * FO_CS_POLY_OF_8
+#ifndef FO_CS_POLY_OF_16
+#define FO_CS_POLY_OF_16 (2 * FO_CS_POLY_OF_8)
+#endif
 // 1: row sums by a P x ones MMA into TMEM (re-reads P from TMEM: ~512 tensor
 // cycles per tile); 0: fp32 row sums in registers, halves combined per item
 #ifndef FO_CS_TC_ROWSUM
@@ -594,7 +598,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         for (int q = 0; q < NCOL / 2; ++q) {
           const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
           float2 e;
-          if ((q & 7) < FO_CS_POLY_OF_8) {
+          if ((q & 15) < FO_CS_POLY_OF_16) {
             e = exp2_poly2(x);
           } else {
             e.x = fast_exp2(x.x);
