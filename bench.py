@@ -242,7 +242,8 @@ def run_reference(args, cfg, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1) tensors, random symbols)",
-            "config": config_json(args, cfg, world, layers),
+            "config": dict(config_json(args, cfg, world, layers),
+                           launch="reference CPU path (compiled _core.pyx + numpy), no GPU"),
             "breakdown_ms": {k: round(x * 1e3, 3) for k, x in parts_sum.items()},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cpu_threads(),
                              "kind": L.kind, "sample": sample},
