@@ -47,7 +47,9 @@ def main():
     res["cublas_gemm_q_dense"] = dict(ms=ms, tflops=gflop / ms / 1e9)
     wq = fo.pack_w_q(w.float().view(H, D, dm).permute(0, 2, 1))
     time.sleep(1)
-    ms = timeit(lambda: fo.project_q(x, wq, None, None, "update", rope=False, fill=None), 3, 10)
+    qo = torch.empty(S, H, D, dtype=torch.bfloat16, device="cuda")
+    ms = timeit(lambda: fo.project_q(x, wq, None, None, "update", rope=False, fill=None, out=qo,
+                                     check=False), 3, 10)
     res["engine_gemm_q_dense_plain"] = dict(ms=ms, tflops=gflop / ms / 1e9)
     print(json.dumps(res))
 
