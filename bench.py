@@ -252,6 +252,13 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def local_device():
+    """This rank's GPU: LOCAL_RANK, or 0 for every rank under FO_BENCH_SHARE_GPU=1."""
+    if os.environ.get("FO_BENCH_SHARE_GPU") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def layers_of(args, cfg):
     return args.layers if args.layers is not None else cfg.get("layers", 1)
 
@@ -283,7 +290,7 @@ def run_b200(args, cfg, rank, world):
     import paper_2509_25401_b200 as fo
     from paper_2509_25401_b200 import _lib
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     group = dist.group.WORLD if world > 1 else None
     S, H, dm = cfg["seq"], cfg["heads"], cfg["d_model"]
@@ -580,8 +587,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # FO_BENCH_BACKEND=gloo with FO_BENCH_SHARE_GPU=1 runs N ranks on one GPU:
+        # a functional check of the sharded path where only one GPU exists
+        dist.init_process_group(os.environ.get("FO_BENCH_BACKEND", "nccl"))
     try:
         run_b200(args, cfg, rank, world)
     finally:
