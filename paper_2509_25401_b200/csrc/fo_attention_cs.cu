@@ -160,7 +160,8 @@ struct ItemCursor {
 };
 
 #ifdef FO_CS_TIMING  // tools/cs_timing.py: per-CTA start/end (globaltimer), SM id, tiles
-__device__ unsigned long long g_cs_timing[12 * 1024];
+__device__ unsigned long long g_cs_timing[16 * 1024];
+__device__ long long g_cs_ph[5 * 1024];
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -248,13 +249,13 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   if (threadIdx.x == 0) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    g_cs_timing[12 * blockIdx.x] = global_ns();
-    g_cs_timing[12 * blockIdx.x + 2] = smid;
-    g_cs_timing[12 * blockIdx.x + 3] = 0;
-    g_cs_timing[12 * blockIdx.x + 8] = 0;
-    g_cs_timing[12 * blockIdx.x + 9] = 0;
-    g_cs_timing[12 * blockIdx.x + 10] = 0;
-    g_cs_timing[12 * blockIdx.x + 11] = 0;
+    g_cs_timing[16 * blockIdx.x] = global_ns();
+    g_cs_timing[16 * blockIdx.x + 2] = smid;
+    g_cs_timing[16 * blockIdx.x + 3] = 0;
+    g_cs_timing[16 * blockIdx.x + 8] = 0;
+    g_cs_timing[16 * blockIdx.x + 9] = 0;
+    g_cs_timing[16 * blockIdx.x + 10] = 0;
+    g_cs_timing[16 * blockIdx.x + 11] = 0;
   }
 #endif
   pdl_release_and_wait();
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #endif
       mbar_wait_small(&bars->q_empty, (qi & 1) ^ 1, p.status);
 #ifdef FO_CS_TIMING
-      if (lane == 0 && k > 0) g_cs_timing[12 * blockIdx.x + 8] += global_ns() - tq0;
+      if (lane == 0 && k > 0) g_cs_timing[16 * blockIdx.x + 8] += global_ns() - tq0;
 #endif
       if (elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         const int n = it.y;
         mbar_wait_small(&bars->q_full, qi & 1, p.status);
 #ifdef FO_CS_TIMING
-        if (lane == 0 && k > 0) g_cs_timing[12 * blockIdx.x + 9] += global_ns() - t_pvl;
+        if (lane == 0 && k > 0) g_cs_timing[16 * blockIdx.x + 9] += global_ns() - t_pvl;
 #endif
         tc_fence_after();
         // QK runs SBUF - 1 tiles ahead of PV; Q is released after the item's last QK
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           const uint32_t c = qk_cnt - la;
           while (!mbar_try_wait(&bars->s_full[c % SBUF], (c / SBUF) & 1)) {
           }
-          if (lane == 0) g_cs_timing[12 * blockIdx.x + 11] += global_ns() - t0;
+          if (lane == 0) g_cs_timing[16 * blockIdx.x + 11] += global_ns() - t0;
         }
 #endif
         if (la == n) commit_q_empty();
@@ -507,6 +508,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #ifdef FO_CS_TIMING
     const bool tmr = threadIdx.x == 128;
     unsigned long long t_mark = 0, g_a = 0, g_b = 0, g_c = 0, n_it = 0;
+    long long g_sw = 0, g_sb = 0, g_st = 0;  // steady-state tiles: S wait, softmax busy (cycles)
+    long long g_ph[5] = {0, 0, 0, 0, 0};      // softmax phases (cycles)
 #endif
     for (int k = 0; have; ++k, ++qi) {
       const int2 it = it_cur;
@@ -520,10 +523,15 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       for (int j = 0; j < n; ++j) {
         const uint32_t sb = qk_seen % SBUF;
 #ifdef FO_CS_TIMING
-        if (tmr && j == 0 && t_mark) g_cs_timing[12 * blockIdx.x + 10] += global_ns() - t_mark;
+        if (tmr && j == 0 && t_mark) g_cs_timing[16 * blockIdx.x + 10] += global_ns() - t_mark;
+#endif
+#ifdef FO_CS_TIMING
+        const long long tw0 = clock64();
 #endif
         mbar_wait_small(&bars->s_full[sb], (qk_seen / SBUF) & 1, p.status);
 #ifdef FO_CS_TIMING
+        const long long tw1 = clock64();
+        if (tmr && j > 0) g_sw += tw1 - tw0;  // steady-state wait for S
         if (tmr && j == 0 && t_mark) {
           const unsigned long long t = global_ns();
           g_c += t - t_mark;  // epilogue end -> first S
@@ -538,6 +546,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < NCH; ++c) reg_fence_cs(u[c]);
+#ifdef FO_CS_TIMING
+        const long long tp1 = clock64();
+#endif
         float sv[NCOL];
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
@@ -572,6 +583,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xa + g * 512) : "memory");
           mo = fmaxf(mo, v);
         }
+#ifdef FO_CS_TIMING
+        asm volatile("" : "+f"(mo));
+        const long long tp2 = clock64();
+#endif
         ++qk_seen;
         const float m_tile = fmaxf(mh, mo) * p.scale_log2;
         bool need = false;
@@ -607,12 +622,19 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           if (!FO_CS_TC_ROWSUM) l2 = fadd2(l2, e);
           pk[q] = pack_bf16x2(e.x, e.y);
         }
+#ifdef FO_CS_TIMING
+        reg_fence_cs(pk);
+        const long long tp3 = clock64();
+#endif
 #if FO_CS_SPLIT == 2
         tmem_st32(sa + half * 32, pk);
 #else
         tmem_st16(sa + half * 16, pk);
 #endif
         tmem_st_wait();
+#ifdef FO_CS_TIMING
+        const long long tp4 = clock64();
+#endif
 #if FO_CS_ODONE_ALL
         // every o_done phase is awaited (PV_{j-1} has long finished by the time
         // P_j is stored, so this costs nothing) and no phase goes unobserved
@@ -649,6 +671,18 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();  // every lane's P / O stores are complete (tcgen05.wait::st above)
         if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+#ifdef FO_CS_TIMING
+        if (tmr && j > 0) {
+          const long long tp5 = clock64();
+          g_sb += tp5 - tw1;  // S landed -> P stored (softmax busy)
+          ++g_st;
+          g_ph[0] += tp1 - tw1;  // S: TMEM -> registers
+          g_ph[1] += tp2 - tp1;  // row max + partner exchange
+          g_ph[2] += tp3 - tp2;  // exponentials + pack
+          g_ph[3] += tp4 - tp3;  // P: registers -> TMEM
+          g_ph[4] += tp5 - tp4;  // rescale check, arrive
+        }
+#endif
       }
       // ---------------- epilogue: this half of O / l -> bf16 -> HBM (+ cache push)
 #ifdef FO_CS_TIMING
@@ -692,7 +726,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       }
       if (r == 0 && half == 0) {
 #ifdef FO_CS_TIMING
-        atomicAdd(&g_cs_timing[12 * blockIdx.x + 3], (unsigned long long)n);
+        atomicAdd(&g_cs_timing[16 * blockIdx.x + 3], (unsigned long long)n);
 #endif
         if (p.pairs && ib < p.t_q)
           atomicAdd(reinterpret_cast<unsigned long long*>(&p.pairs[h]),
@@ -808,10 +842,14 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     }
 #ifdef FO_CS_TIMING
     if (tmr) {
-      g_cs_timing[12 * blockIdx.x + 4] = g_a;
-      g_cs_timing[12 * blockIdx.x + 5] = g_b;
-      g_cs_timing[12 * blockIdx.x + 6] = g_c;
-      g_cs_timing[12 * blockIdx.x + 7] = n_it;
+      g_cs_timing[16 * blockIdx.x + 4] = g_a;
+      g_cs_timing[16 * blockIdx.x + 5] = g_b;
+      g_cs_timing[16 * blockIdx.x + 6] = g_c;
+      g_cs_timing[16 * blockIdx.x + 7] = n_it;
+      g_cs_timing[16 * blockIdx.x + 12] = g_sw;
+      g_cs_timing[16 * blockIdx.x + 13] = g_sb;
+      g_cs_timing[16 * blockIdx.x + 14] = g_st;
+      for (int k = 0; k < 5; ++k) g_cs_ph[5 * blockIdx.x + k] = g_ph[k];
     }
 #endif
 #if FO_CS_TMA_OUT
@@ -825,7 +863,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
   __syncthreads();
   if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal into it
 #ifdef FO_CS_TIMING
-  if (threadIdx.x == 0) g_cs_timing[12 * blockIdx.x + 1] = global_ns();
+  if (threadIdx.x == 0) g_cs_timing[16 * blockIdx.x + 1] = global_ns();
 #endif
   if (warp == 1) {
     tc_fence_after();
@@ -836,7 +874,10 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #ifdef FO_CS_TIMING
 extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigned long long* out,
                                                                        int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 12 * n);
+  return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 16 * n);
+}
+extern "C" __attribute__((visibility("default"))) int fo_debug_cs_phases(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cs_ph, sizeof(long long) * 5 * n);
 }
 #endif
 

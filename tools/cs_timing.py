@@ -30,14 +30,14 @@ for _ in range(5):
 torch.cuda.synchronize()
 lib = _lib.load()
 n = 148
-buf = (ctypes.c_ulonglong * (12 * 1024))()
+buf = (ctypes.c_ulonglong * (16 * 1024))()
 assert lib.fo_debug_cs_timing(buf, 1024) == 0
-raw = [int(v) for v in buf[:12 * n]]
+raw = [int(v) for v in buf[:16 * n]]
 raw0 = [v - (1 << 64) if v >= (1 << 63) else v for v in raw]
 qk_to_s = np.array([float('nan')] * n)
 for b in range(n):
-    raw[12 * b + 10] = 0
-a = np.array(raw, dtype=np.int64).reshape(n, 12)
+    raw[16 * b + 10] = 0
+a = np.array(raw, dtype=np.int64).reshape(n, 16)
 t0 = a[:, 0].min()
 start, end, sm, tiles = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2], a[:, 3]
 ga, gb, gc, nit = a[:, 4] / 1e3, a[:, 5] / 1e3, a[:, 6] / 1e3, np.maximum(a[:, 7], 1)
@@ -53,7 +53,16 @@ print(f"per item (us): last P -> last PV done {np.mean(ga / nit):.2f}, epilogue 
       f"boundary share of the span {np.mean(ga + gb + gc) / end.max():.2%}")
 print(f"per item (us): producer waits q_empty {np.mean(a[:, 8] / 1e3 / nit):.2f}; "
       f"MMA last PV issued -> next Q landed {np.mean(a[:, 9] / 1e3 / nit):.2f}")
-print(f"per item (us): softmax epilogue end -> reaches the first S wait {np.mean(np.array([raw0[12 * b + 10] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
-print(f"per item (us): first QK issued -> its s_full completes (MMA warp polling) {np.mean(np.array([raw0[12 * b + 11] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
+print(f"per item (us): softmax epilogue end -> reaches the first S wait {np.mean(np.array([raw0[16 * b + 10] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
+print(f"per item (us): first QK issued -> its s_full completes (MMA warp polling) {np.mean(np.array([raw0[16 * b + 11] for b in range(n)], dtype=np.float64) / 1e3 / np.maximum(nit - 1, 1)):.2f}")
 order = np.argsort(sm)
 print("by SM (sm: ns/tile):", " ".join(f"{s}:{r:.0f}" for s, r in zip(sm[order][:148:8], rate[order][:148:8])))
+st = np.maximum(a[:, 14], 1)
+print(f"steady-state tile (cycles, softmax thread 128): waiting for S {np.mean(a[:, 12] / st):.0f}, "
+      f"S landed -> P stored {np.mean(a[:, 13] / st):.0f}, tiles/CTA {np.mean(a[:, 14]):.0f}")
+ph = (ctypes.c_longlong * (5 * 1024))()
+if hasattr(lib, "fo_debug_cs_phases") and lib.fo_debug_cs_phases(ph, 1024) == 0:
+    P = np.array(ph[:5 * n], dtype=np.int64).reshape(n, 5) / st[:, None]
+    names = ["S tmem->reg", "max+exchange", "exp+pack", "P reg->tmem", "check+arrive"]
+    print("softmax phases (cycles/tile): " + ", ".join(f"{k} {v:.0f}" for k, v in zip(names, P.mean(0))))
+
