@@ -613,7 +613,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         for (int q = 0; q < NCOL / 2; ++q) {
           const float2 x = ffma2(make_float2(sv[2 * q], sv[2 * q + 1]), sc2, nm2);
           float2 e;
+#ifdef FO_CS_POLY_MASK  // which pairs of every 16 take the polynomial (interleave pattern)
+          if ((FO_CS_POLY_MASK >> (q & 15)) & 1) {
+#else
           if ((q & 15) < FO_CS_POLY_OF_16) {
+#endif
             e = exp2_poly2(x);
           } else {
             e.x = fast_exp2(x.x);
