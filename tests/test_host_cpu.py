@@ -134,3 +134,26 @@ def test_no_oracle_in_product():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+
+
+def test_building_block_entry_points_validate_without_gpu():
+    """The reference building blocks' C entry points reject bad arguments with
+    the reference exception classes before any launch."""
+    from paper_2509_25401_b200 import _lib
+    from paper_2509_25401_b200.errors import BoundsError, ParameterError, ShapeError
+
+    with pytest.raises(ParameterError):  # null operands
+        _lib.call("fo_online_softmax_update", None, None, None, None, None, 4, 4, 4, None, None,
+                  None, None)
+    with pytest.raises(ParameterError):  # pool < 1 (tensor.py:119-120)
+        _lib.call("fo_mean_pool_blocks", 8, 4, 4, 0, 8, None)
+    with pytest.raises(ShapeError):  # rope needs an even feature dim (tensor.py:91-92)
+        _lib.call("fo_rope", 8, 8, 8, 4, 5, 8, None)
+    with pytest.raises(ParameterError):  # tau_q outside [0, 1] (policy.py:101-102)
+        _lib.call("fo_policy_select_cached", 8, 8, 1, 4, 1.5, 8, None)
+    with pytest.raises(ParameterError):  # tau_kv outside [0, 1] (policy.py:136-137)
+        _lib.call("fo_policy_select_skip", 8, 8, 1, 4, 4, 0, -0.5, 1, 8, None)
+    with pytest.raises(ParameterError):  # forecast orders outside [1, 8]
+        _lib.call("fo_forecast_entry", 8, 16, 0, 8, 8, None)
+    with pytest.raises(BoundsError):  # entry outside the cache
+        _lib.call("fo_cache_push_tile", 16, 16, 16, 256, 2, 128, 2, 1, 2, 0, None)
