@@ -185,6 +185,17 @@ FO_API int fo_gemm_o_dispatch_rows(const void* o, const void* w_outt, const void
                                    int block_begin, int block_end, int max_sms, void* out,
                                    void* stream);
 
+/* The dispatch step's three projections in ONE launch (pipeline.py:223-234 +
+ * gemm.py:44-93): q (GEMM-Q, RMSNorm + RoPE; only the plan's active tiles, or
+ * every tile with dense=1), k (dense, RMSNorm + RoPE with k_norm) and v (dense,
+ * plain) from one read of x. w_qkvt: bf16 [3*heads*128, d_model] = [W_q^T;
+ * W_k^T; W_v^T]. heads <= 32. */
+FO_API int fo_gemm_qkv(const void* x, int seq, int d_model, const void* w_qkvt, int heads,
+                       int head_dim, const float* q_norm, const float* k_norm,
+                       const float* rope_cos, const float* rope_sin, float eps,
+                       const void* plan_ws, int dense, void* q_out, void* k_out, void* v_out,
+                       void* stream);
+
 /* Stale-symbol check (gemm.py:201-209): STATE if the decoded cache bits differ. */
 FO_API int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
                           int pool_n, uint32_t* status, void* stream);

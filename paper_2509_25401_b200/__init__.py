@@ -48,9 +48,11 @@ from .gemm import (
     GemmCounters,
     pack_w_out,
     pack_w_q,
+    pack_w_qkv,
     project_out_dispatch,
     project_out_update,
     project_q,
+    project_qkv,
     rope_tables,
 )
 from .pipeline import (

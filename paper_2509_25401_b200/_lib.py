@@ -47,6 +47,7 @@ SIGNATURES = {
     "fo_cache_push": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
     "fo_cache_push_tile": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P],
     "fo_gemm_q": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _F, _P, _I, _P, _P],
+    "fo_gemm_qkv": [_P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _F, _P, _I, _P, _P, _P, _P],
     "fo_gemm_o_update": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "fo_gemm_o_dispatch": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
     "fo_gemm_o_dispatch_rows": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P],

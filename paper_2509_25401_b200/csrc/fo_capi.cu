@@ -438,9 +438,60 @@ int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, 
   p.rope_sin = rope_sin;
   p.eps = eps;
   p.q = static_cast<__nv_bfloat16*>(q_out);
+  p.qkv = 0;
+  p.k_out = p.v_out = nullptr;
+  p.k_norm = nullptr;
   // one persistent launch on CTA pairs for both phases (fo_gemm.cu gemm_q2_kernel)
   launch_gemm_q2(xm, wm, wm64, p, (cudaStream_t)stream);
   return check_launch("gemm_q");
+}
+
+int fo_gemm_qkv(const void* x, int seq, int d_model, const void* w_qkvt, int heads, int head_dim,
+                const float* q_norm, const float* k_norm, const float* rope_cos,
+                const float* rope_sin, float eps, const void* plan_ws, int dense, void* q_out,
+                void* k_out, void* v_out, void* stream) {
+  int rc = check_head_dim(head_dim);
+  if (rc) return rc;
+  if (d_model % 64 != 0 || d_model < 64) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 64");
+  if ((rc = check_align32(q_out, "q_out")) || (rc = check_align32(k_out, "k_out")) ||
+      (rc = check_align32(v_out, "v_out")))
+    return rc;
+  if (!x || !w_qkvt || !q_out || !k_out || !v_out)
+    return fail(FO_ERR_PARAM, "gemm_qkv: null pointer");
+  // Q's and K's norm weights share the 64-head shared-memory table
+  if (heads < 1 || heads > 32) return fail(FO_ERR_PARAM, "gemm_qkv: heads must be in [1, 32]");
+  if (!dense && !plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
+  CUtensorMap xm, wm, wm64;
+  const uint64_t rows_w = 3 * (uint64_t)heads * kTile;
+  if ((rc = make_map(&xm, x, seq, d_model, 128, "x"))) return rc;
+  if ((rc = make_map(&wm, w_qkvt, rows_w, d_model, 128, "w_qkv"))) return rc;
+  if ((rc = make_map(&wm64, w_qkvt, rows_w, d_model, 64, "w_qkv"))) return rc;
+  const int t_q = ceil_div_d(seq, kTile);
+  GemmQParams p;
+  p.S = seq;
+  p.dm = d_model;
+  p.H = heads;
+  p.t_q = t_q;
+  p.dense = dense;
+  if (!dense) {
+    PlanView pv = plan_view(plan_ws, heads, t_q);
+    p.jobs = pv.gq_jobs;
+    p.n_jobs = pv.counts + 7;
+  } else {
+    p.jobs = nullptr;
+    p.n_jobs = nullptr;
+  }
+  p.norm_w = q_norm;
+  p.rope_cos = rope_cos;
+  p.rope_sin = rope_sin;
+  p.eps = eps;
+  p.q = static_cast<__nv_bfloat16*>(q_out);
+  p.qkv = 1;
+  p.k_out = static_cast<__nv_bfloat16*>(k_out);
+  p.v_out = static_cast<__nv_bfloat16*>(v_out);
+  p.k_norm = k_norm;
+  launch_gemm_q2(xm, wm, wm64, p, (cudaStream_t)stream);
+  return check_launch("gemm_qkv");
 }
 
 static int gemm_o_common(const void* o, const void* cache, const void* w_outt, int seq, int heads,

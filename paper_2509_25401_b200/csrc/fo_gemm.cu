@@ -222,12 +222,14 @@ namespace gemm {
 // 32-column chunks, loading the row's rotary chunk once for both heads
 // (prefetched a chunk ahead) and the norm weights from shared memory.
 // release() hands the accumulator back to the MMA warp after its last read.
+// Per projection (segment): out is its [S, H*128] output, norm / rope its
+// epilogue (Q, K: RMSNorm + RoPE; V: plain), nw_u32 its norm weights' smem.
 template <typename Release>
 __device__ __forceinline__ void q_epilogue_job(const GemmQParams& p, uint32_t ta0, int r, int i,
-                                               int h1, int h2, uint32_t nw_u32, Release release) {
+                                               int h1, int h2, uint32_t nw_u32,
+                                               __nv_bfloat16* out, bool norm, bool rope,
+                                               Release release) {
   const size_t HD = (size_t)p.H * 128;
-  const bool rope = p.rope_cos != nullptr;
-  const bool norm = p.norm_w != nullptr;
   const int row = i * BM + r;
   const bool row_ok = row < p.S;
   const int nh = h2 >= 0 ? 2 : 1;
@@ -314,7 +316,7 @@ __device__ __forceinline__ void q_epilogue_job(const GemmQParams& p, uint32_t ta
           }
         }
       }
-      gemm::store_bf16x32(p.q + (size_t)row * HD + (size_t)h * 128 + cc * 32, o);
+      gemm::store_bf16x32(out + (size_t)row * HD + (size_t)h * 128 + cc * 32, o);
     }
   }
 }
@@ -376,16 +378,25 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   pdl_release_and_wait();
-  if (p.norm_w) {
-    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x)
-      reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
+  if (p.norm_w || (p.qkv && p.k_norm)) {
+    // Q's norm weights at heads [0, H), K's (fused launch) at [H, 2H)
+    for (int e = threadIdx.x; e < p.H * 32; e += blockDim.x) {
+      if (p.norm_w)
+        reinterpret_cast<float4*>(nw_smem)[e] = __ldg(reinterpret_cast<const float4*>(p.norm_w) + e);
+      if (p.qkv && p.k_norm)
+        reinterpret_cast<float4*>(nw_smem)[p.H * 32 + e] =
+            __ldg(reinterpret_cast<const float4*>(p.k_norm) + e);
+    }
     __syncthreads();
   }
   const uint32_t tbase = bars->tmem_base;
   const int nph = p.H >> 1;            // full head pairs
   const int npj = nph + (p.H & 1);     // dense jobs per block pair (odd last head: N=128)
   const int nbp = (p.t_q + 1) >> 1;    // block pairs
-  const int n_cjobs = p.dense ? nbp * npj : *p.n_jobs;
+  // fused launch: the dense K and V jobs (block-pair-major, K then V head pairs
+  // of each block pair) come first, then Q's (dense or the plan's sparse list)
+  const int n_kv = p.qkv ? 2 * nbp * npj : 0;
+  const int n_cjobs = n_kv + (p.dense ? nbp * npj : *p.n_jobs);
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   // round rr of cluster cid takes job rr*ncl + cid, snaking (reversed on odd
   // rounds): the plan lists the sparse jobs by cost class (N = 256, then
@@ -395,16 +406,26 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   const int nkb = p.dm / BK;
   // job -> this CTA's block i, head h and width (n256: heads h, h+1); false: no
   // block for this CTA (it loads zero rows past the end and skips its epilogue)
-  auto job = [&](int c, int& i, int& h, bool& n256) -> bool {
+  // seg: 0 Q, 1 K, 2 V (rows seg*H*128.. of the fused weight)
+  auto job = [&](int c, int& i, int& h, bool& n256, int& seg) -> bool {
     int i0, i1;
-    if (p.dense) {  // block-pair-major
+    seg = 0;
+    if (c < n_kv) {  // fused K / V: block-pair-major, then K / V, then head pair
+      const int bp = c / (2 * npj), r2 = c - bp * 2 * npj, r = r2 % npj;
+      seg = 1 + r2 / npj;
+      i0 = 2 * bp;
+      i1 = 2 * bp + 1 < p.t_q ? 2 * bp + 1 : -1;
+      h = 2 * r;
+      n256 = r < nph;
+    } else if (p.dense) {  // block-pair-major
+      c -= n_kv;
       const int bp = c / npj, r = c - bp * npj;
       i0 = 2 * bp;
       i1 = 2 * bp + 1 < p.t_q ? 2 * bp + 1 : -1;
       h = 2 * r;
       n256 = r < nph;
     } else {
-      const int2 code = p.jobs[c];
+      const int2 code = p.jobs[c - n_kv];
       i0 = code.x & 0xFFFF;
       i1 = (code.x >> 16) - 1;
       h = code.y & 0xFF;
@@ -421,10 +442,11 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h;
+      int i, h, seg;
       bool n256;
-      job(c, i, h, n256);  // a missing block loads zero rows (coordinates past the end)
+      job(c, i, h, n256, seg);  // a missing block loads zero rows (coordinates past the end)
       const uint32_t b_bytes = n256 ? B_BYTES : B_BYTES / 2;
+      h += seg * p.H;  // the projection's rows of the (fused) weight
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
@@ -450,9 +472,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h;
+      int i, h, seg;
       bool n256;
-      job(c, i, h, n256);
+      job(c, i, h, n256, seg);
       const uint32_t idesc = n256 ? idesc256 : idesc128;
       const int acc = t & 1;
       mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
@@ -485,9 +507,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h;
+      int i, h, seg;
       bool n256;
-      const bool mine = job(c, i, h, n256);
+      const bool mine = job(c, i, h, n256, seg);
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -496,9 +518,13 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&bars->tempty[acc], 0);
       };
-      if (mine)
-        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h, n256 ? h + 1 : -1, nw_u32,
-                             release);
+      if (mine) {
+        __nv_bfloat16* out = seg == 0 ? p.q : (seg == 1 ? p.k_out : p.v_out);
+        const bool norm = seg == 0 ? p.norm_w != nullptr : (seg == 1 && p.k_norm != nullptr);
+        const bool rope = seg < 2 && p.rope_cos != nullptr;
+        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h, n256 ? h + 1 : -1,
+                             nw_u32 + (seg == 1 ? p.H * 128 * 4 : 0), out, norm, rope, release);
+      }
       else
         release();
       ++t;

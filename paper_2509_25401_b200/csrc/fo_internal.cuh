@@ -204,6 +204,12 @@ struct GemmQParams {
   const float* rope_sin;  // [S, 64]
   float eps;
   __nv_bfloat16* q;  // [S, H*128]
+  // fused dispatch projection (fo_gemm_qkv): W holds [W_q; W_k; W_v] and the
+  // launch also runs the dense K (RMSNorm + RoPE) and V (plain) projections
+  int qkv;
+  __nv_bfloat16* k_out;  // [S, H*128]
+  __nv_bfloat16* v_out;  // [S, H*128]
+  const float* k_norm;   // [H, 128]
 };
 // GEMM-Q on CTA pairs (cta_group::2), persistent: every tile of the dense phase
 // and of the sparse phase in one launch. xm: x with a 128-row box; wm / wm64:

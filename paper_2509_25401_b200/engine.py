@@ -36,7 +36,7 @@ from ._runtime import TILE, Status, stream_ptr
 from .attention import FeatureCache, dense_attention_update, sparse_attention
 from .costs import StepCost, account_run
 from .errors import ParameterError
-from .gemm import CachedBias, project_out_dispatch, project_out_update, project_q
+from .gemm import CachedBias, project_out_dispatch, project_out_update, project_q, project_qkv
 from .pipeline import LayerParams, project_kv, shard_heads
 from .plan import Plan
 from .policy import generate_masks_heads, ramp_threshold
@@ -276,9 +276,13 @@ class _Layer:
     # ------------------------------------------------------------------ phases
     def update(self, x, t_step, status):
         cfg, p = self.cfg, self.params
-        project_q(x, p.w_q, p.q_norm, None, "update", out=self.q, fill=None, status=status,
-                  check=False)
-        project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
+        if p.w_qkv is not None:  # q, k, v in one launch
+            project_qkv(x, p.w_qkv, p.q_norm, p.k_norm, None, "update", q_out=self.q,
+                        k_out=self.k, v_out=self.v, status=status, check=False)
+        else:
+            project_q(x, p.w_q, p.q_norm, None, "update", out=self.q, fill=None, status=status,
+                      check=False)
+            project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
         tau_q = ramp_threshold(cfg.tau_q, t_step, cfg.warmup)
         tau_kv = ramp_threshold(cfg.tau_kv, t_step, cfg.warmup)
         generate_masks_heads(self.q, self.k, pool_n=cfg.pool_n, n_text=cfg.n_text, tau_q=tau_q,
@@ -318,9 +322,13 @@ class _Layer:
 
     def dispatch(self, x, elapsed_k, status):
         cfg, p = self.cfg, self.params
-        project_q(x, p.w_q, p.q_norm, self.sym, "dispatch", out=self.q, plan=self.plan_c,
-                  status=status, check=False)
-        project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
+        if p.w_qkv is not None:  # active q tiles, k and v in one launch
+            project_qkv(x, p.w_qkv, p.q_norm, p.k_norm, self.sym, "dispatch", q_out=self.q,
+                        k_out=self.k, v_out=self.v, plan=self.plan_c, status=status, check=False)
+        else:
+            project_q(x, p.w_q, p.q_norm, self.sym, "dispatch", out=self.q, plan=self.plan_c,
+                      status=status, check=False)
+            project_kv(x, p, k_out=self.k, v_out=self.v, check=False)
         sparse_attention(self.q, self.k, self.v, self.sym, self.cache, None, elapsed_k,
                          cfg.interval_n, cfg.order_d, mode="bias", out=self.o, plan=self.plan_c,
                          pairs=self.pairs, status=status, check=False)

@@ -157,6 +157,62 @@ def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, 
     return out
 
 
+def pack_w_qkv(w_q, w_k, w_v):
+    """[W_q^T; W_k^T; W_v^T] bf16 [3*heads*128, d_model] for the fused
+    projection (one weight, one TMA map)."""
+    q, k, v = pack_w_q(w_q), pack_w_q(w_k), pack_w_q(w_v)
+    if not (q.heads == k.heads == v.heads and q.d_model == k.d_model == v.d_model):
+        raise ShapeError("w_q / w_k / w_v disagree on heads or d_model")
+    return PackedWeight(torch.cat([q.t, k.t, v.t], 0).contiguous(), q.heads, q.d_model)
+
+
+def project_qkv(x, w_qkv, q_norm, k_norm, symbols, phase, *, positions=None, eps=1e-6,
+                q_out=None, k_out=None, v_out=None, fill=None, stream=None, status=None,
+                check=True, plan=None):
+    """The dispatch step's three projections (pipeline.py:223-234 with
+    gemm.py:44-93) in ONE launch that reads x once: q = rope(rms_norm(x W_q))
+    for the active tiles (every tile in the update phase), k = rope(rms_norm(x
+    W_k)) and v = x W_v densely. w_qkv: pack_w_qkv(...). Returns (q, k, v)."""
+    require_cuda()
+    if phase not in ("update", "dispatch"):
+        raise ParameterError(f"unknown phase {phase!r}")
+    x = as_device(x, torch.bfloat16, "x")
+    if x.dim() != 2:
+        raise ShapeError(f"x: expected a 2-D matrix, got shape {tuple(x.shape)}")
+    n, dm = x.shape
+    if dm != w_qkv.d_model:
+        raise ShapeError(f"x width {dm} != projection input {w_qkv.d_model}")
+    heads = w_qkv.heads
+    if tuple(w_qkv.t.shape) != (3 * heads * TILE, dm):
+        raise ShapeError("w_qkv: expected the packed [W_q; W_k; W_v] (pack_w_qkv)")
+    t_q = ceil_div(n, TILE)
+    if check:  # gemm.py:64 as_matrix(x)
+        check_finite(x, "x", status, stream=stream)
+    qn, kn = _norm(q_norm, heads), _norm(k_norm, heads)
+    cs, sn = rope_tables(n, positions, x.device)
+    outs = []
+    for name, o in (("q_out", q_out), ("k_out", k_out), ("v_out", v_out)):
+        if o is None:
+            # q's skipped tiles keep `fill`; k and v are written everywhere
+            f = fill if (name == "q_out" and fill is not None) else 0.0
+            o = torch.full((n, heads, TILE), float(f), dtype=torch.bfloat16, device=x.device)
+        else:
+            check_out(o, name, (n, heads, TILE), device=x.device)
+        outs.append(o)
+    if phase == "dispatch":
+        if symbols is None or symbols.heads != heads or symbols.rows != t_q:
+            raise ShapeError(f"symbols must cover {heads} heads x {t_q} blocks")
+        if plan is None:
+            plan = symbols.plan(status=status, stream=stream, check=check)
+    else:
+        plan = None
+    _lib.call("fo_gemm_qkv", x.data_ptr(), n, dm, w_qkv.t.data_ptr(), heads, TILE, qn.data_ptr(),
+              kn.data_ptr(), cs.data_ptr(), sn.data_ptr(), float(eps),
+              None if plan is None else plan.ptr(), 1 if phase == "update" else 0,
+              outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(), stream_ptr(stream))
+    return tuple(outs)
+
+
 # ---------------------------------------------------------------------------
 # GEMM-O
 # ---------------------------------------------------------------------------

@@ -14,6 +14,7 @@ cached bias) are summed by one all-reduce — exact by linearity of the
 projection and the forecast.
 """
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -21,7 +22,8 @@ import torch
 from ._runtime import TILE, Status, as_device
 from .attention import FeatureCache, dense_attention_update, sparse_attention
 from .errors import ParameterError, StateError
-from .gemm import pack_w_out, pack_w_q, project_out_dispatch, project_out_update, project_q
+from .gemm import (pack_w_out, pack_w_q, pack_w_qkv, project_out_dispatch, project_out_update,
+                   project_q, project_qkv)
 from .symbols import ceil_div
 
 
@@ -51,6 +53,15 @@ class LayerParams:
     @property
     def heads(self):
         return self.w_q.heads
+
+    @property
+    def w_qkv(self):
+        """[W_q; W_k; W_v] packed once for the fused projection (None above
+        32 heads per rank, where the three launches are used)."""
+        if not hasattr(self, "_w_qkv"):
+            fused = self.heads <= 32 and os.environ.get("FO_FUSED_QKV", "1") != "0"
+            self._w_qkv = pack_w_qkv(self.w_q, self.w_k, self.w_v) if fused else None
+        return self._w_qkv
 
 
 @dataclass
@@ -94,8 +105,11 @@ def update_step(state, x, symbols_next, order_d, *, group=None, check=True, poli
     when symbols_next is None, else from the caller."""
     x = as_device(x, torch.bfloat16, "x")
     p = state.params
-    q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None, check=check)
-    k, v = project_kv(x, p, check=False)
+    if p.w_qkv is not None:  # q, k, v in one launch (one read of x)
+        q, k, v = project_qkv(x, p.w_qkv, p.q_norm, p.k_norm, None, "update", check=check)
+    else:
+        q = project_q(x, p.w_q, p.q_norm, None, "update", fill=None, check=check)
+        k, v = project_kv(x, p, check=False)
     if symbols_next is None:
         if policy is None:
             raise ParameterError("update_step needs symbols_next or a MaskPolicy")
@@ -164,9 +178,14 @@ def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check
     x = as_device(x, torch.bfloat16, "x")
     p = state.params
     b = bufs or {}
-    q = project_q(x, p.w_q, p.q_norm, state.symbols, "dispatch", fill=fill, out=b.get("q"),
-                  check=check)
-    k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"), check=False)
+    if p.w_qkv is not None:  # q (active tiles), k and v in one launch (one read of x)
+        q, k, v = project_qkv(x, p.w_qkv, p.q_norm, p.k_norm, state.symbols, "dispatch",
+                              q_out=b.get("q"), k_out=b.get("k"), v_out=b.get("v"), fill=fill,
+                              check=check)
+    else:
+        q = project_q(x, p.w_q, p.q_norm, state.symbols, "dispatch", fill=fill, out=b.get("q"),
+                      check=check)
+        k, v = project_kv(x, p, k_out=b.get("k"), v_out=b.get("v"), check=False)
     o = sparse_attention(q, k, v, state.symbols, state.cache, None, elapsed_k, interval_n, order_d,
                          mode="bias", fill=fill, out=b.get("o"), check=check)
     if group is not None and chunks > 1:

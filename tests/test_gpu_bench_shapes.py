@@ -335,3 +335,35 @@ def test_attention_c2_flux(sparsity):
     for h in range(H):
         np.fill_diagonal(sb[h], True)
     _attention_check(m, 4608, H, cb, sb, [0, 11, 23], 61)
+
+
+def test_fused_qkv_projection_matches_separate_launches():
+    """fo_gemm_qkv (one launch: the plan's active Q tiles + dense K and V)
+    equals the three separate projections bit for bit (same tiles, same K
+    order), in the dispatch and the update phase, at the bench's shape."""
+    import torch
+
+    m = fo()
+    rng = np.random.default_rng(17)
+    S, H, dm, T = 4096 + 128 * 3, 24, 3072, 128
+    t = -(-S // T)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(S, dm, device="cuda", generator=g).bfloat16()
+    w = [torch.randn(H, dm, T, device="cuda", generator=g) * dm ** -0.5 for _ in range(3)]
+    qn = 1 + 0.05 * torch.randn(H, T, device="cuda", generator=g)
+    kn = 1 + 0.05 * torch.randn(H, T, device="cuda", generator=g)
+    params = m.LayerParams.from_reference(w[0], w[1], w[2], qn, kn,
+                                          torch.randn(H, T, dm, device="cuda") * T ** -0.5)
+    active = rng.random((H, t)) >= 0.6
+    sym = m.encode_symbols(active, np.ones((H, t, t), bool), 1)
+    for phase, sy in (("dispatch", sym), ("update", None)):
+        q, k, v = m.project_qkv(x, params.w_qkv, qn, kn, sy, phase, fill=float("nan"))
+        q0 = m.project_q(x, params.w_q, qn, sy, phase, fill=float("nan"))
+        k0, v0 = m.project_kv(x, params)
+        torch.cuda.synchronize()
+        assert torch.equal(k, k0) and torch.equal(v, v0)
+        rows = torch.ones(S, H, dtype=torch.bool, device="cuda")
+        if phase == "dispatch":
+            rows = torch.from_numpy(np.repeat(active.T, T, axis=0)[:S]).cuda()
+            assert torch.isnan(q[~rows]).all()  # skipped tiles keep the fill
+        assert torch.equal(q[rows], q0[rows])
