@@ -41,6 +41,11 @@ o = torch.randn(S, H, T, device="cuda", generator=g).bfloat16()
 qo = torch.empty(S, H, T, dtype=torch.bfloat16, device="cuda")
 out = torch.empty(S, dm, dtype=torch.bfloat16, device="cuda")
 full = np.ones((H, t, t), bool)
+if "qkv" in ops:
+    wraw = [torch.randn(H, dm, T, device="cuda", generator=g) * dm ** -0.5 for _ in range(3)]
+    wqkv, wk = fo.pack_w_qkv(*wraw), fo.pack_w_q(wraw[1])
+    ko, vo = torch.empty_like(qo), torch.empty_like(qo)
+    dsym = fo.encode_symbols(np.ones((H, t), bool), full, 1)
 res = {}
 for order in [int(v) for v in a.orders.split(",")]:
     fc = fo.FeatureCache(H, t, order, seq=S)
@@ -52,6 +57,16 @@ for order in [int(v) for v in a.orders.split(",")]:
         if "q" in ops and order == int(a.orders.split(",")[0]):
             res[f"q@{r}"] = round(timeit(lambda: fo.project_q(x, wq, norm, sym, "dispatch", out=qo,
                                                               fill=None, check=False)), 4)
+        if "qkv" in ops and order == int(a.orders.split(",")[0]):
+            # the dispatch step's projections: one fused launch vs Q + K + V launches
+            res[f"qkv@{r}"] = round(timeit(lambda: fo.project_qkv(
+                x, wqkv, norm, norm, sym, "dispatch", q_out=qo, k_out=ko, v_out=vo,
+                check=False)), 4)
+            res[f"q+k+v@{r}"] = round(timeit(lambda: (
+                fo.project_q(x, wq, norm, sym, "dispatch", out=qo, fill=None, check=False),
+                fo.project_q(x, wk, norm, dsym, "dispatch", out=ko, fill=None, check=False),
+                fo.project_q(x, wk, None, dsym, "dispatch", out=vo, fill=None, rope=False,
+                             check=False))), 4)
         _, bias = fo.project_out_update(o, wo, sym, fc, order)
         if "disp" in ops:
             res[f"disp@{r}/D{order}"] = round(timeit(lambda: fo.project_out_dispatch(
