@@ -1,6 +1,7 @@
 // C ABI (include/flashomni_b200.h): argument validation, TMA descriptor
 // construction and kernel launches. No allocation, no synchronisation.
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdarg>
@@ -20,6 +21,17 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 thread_local char g_err[512] = "";
+
+// One NVTX range per compute entry point, named after it (header-only NVTX3:
+// a no-op unless a tool such as ncu / nsys injects itself). Lets a profiler
+// select an operator's kernels: ncu --nvtx --nvtx-include "fo_sparse_attention/"
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define FO_RANGE() NvtxRange fo_nvtx_range_(__func__)
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -185,6 +197,7 @@ void fo_plan_offsets(int heads, int rows, size_t offsets[7]) {
 int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int heads, int rows,
                       int cols, int pool_n, uint8_t* s_c, uint8_t* s_s, uint32_t* status,
                       void* stream) {
+  FO_RANGE();
   int rc = check_symbol_dims(heads, rows, cols, pool_n);
   if (rc) return rc;
   const int comp_rows = ceil_div_d(rows, pool_n);
@@ -199,6 +212,7 @@ int fo_encode_symbols(const uint8_t* cache_bits, const uint8_t* skip_bits, int h
 
 int fo_decode_symbols(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols,
                       int pool_n, uint8_t* active, uint8_t* pair_bits, void* stream) {
+  FO_RANGE();
   int rc = check_symbol_dims(heads, rows, cols, pool_n);
   if (rc) return rc;
   const long long total = (long long)heads * rows * cols;
@@ -212,6 +226,7 @@ int fo_decode_symbols(const uint8_t* s_c, const uint8_t* s_s, int heads, int row
 int fo_plan(const uint8_t* s_c, const uint8_t* s_s, int heads, int rows, int cols, int pool_n,
             int dense, const int32_t* valid, int order_d, void* plan_ws, uint32_t* status,
             void* stream) {
+  FO_RANGE();
   int rc = check_symbol_dims(heads, rows, cols, pool_n);
   if (rc) return rc;
   if (!plan_ws) return fail(FO_ERR_PARAM, "plan workspace is NULL");
@@ -318,6 +333,7 @@ int fo_sparse_attention(const void* q, const void* k, const void* v, int seq, in
                         const void* plan_ws, float scale, int update_mode, void* out, void* cache,
                         int32_t* valid, int order_d, int64_t* pairs, uint32_t* status,
                         void* stream) {
+  FO_RANGE();
   return attention_common(q, k, v, seq, heads, head_dim, s_s, rows, cols, pool_n, plan_ws, scale,
                           update_mode, out, cache, valid, order_d, pairs, status, nullptr, nullptr,
                           nullptr, stream);
@@ -328,6 +344,7 @@ int fo_sparse_attention_reuse(const void* q, const void* k, const void* v, int s
                               const void* plan_ws, float scale, const void* cache,
                               const int32_t* valid, int order_d, const float* coef, void* out,
                               int64_t* pairs, uint32_t* status, void* stream) {
+  FO_RANGE();
   if (!cache || !valid || !coef)
     return fail(FO_ERR_STATE, "materialize mode needs the feature cache, its valid orders and coef");
   return attention_common(q, k, v, seq, heads, head_dim, s_s, rows, cols, pool_n, plan_ws, scale,
@@ -338,6 +355,7 @@ int fo_sparse_attention_reuse(const void* q, const void* k, const void* v, int s
 int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim, int rows,
                             int order_d, const void* plan_ws, const int32_t* valid,
                             const float* coef, void* out, void* stream) {
+  FO_RANGE();
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
@@ -355,6 +373,7 @@ int fo_forecast_materialize(const void* cache, int seq, int heads, int head_dim,
 
 int fo_check_finite(const void* data, long long rows, int cols, const void* plan_ws, int heads,
                     uint32_t* status, void* stream) {
+  FO_RANGE();
   if (!data || !status) return fail(FO_ERR_PARAM, "check_finite: NULL operand");
   if (cols % 8 != 0) return fail(FO_ERR_SHAPE, "check_finite: %d columns, need a multiple of 8", cols);
   if ((reinterpret_cast<uintptr_t>(data) & 15) != 0)
@@ -370,6 +389,7 @@ int fo_check_finite(const void* data, long long rows, int cols, const void* plan
 
 int fo_synthetic_x(const float* x0, const float* a, const float* b, size_t n, int kind, float c1,
                    float c2, float s, void* out, void* stream) {
+  FO_RANGE();
   if (!x0 || !a || !b || !out) return fail(FO_ERR_PARAM, "synthetic_x: NULL operand");
   if (kind < 0 || kind > 2) return fail(FO_ERR_PARAM, "synthetic_x: unknown workload kind %d", kind);
   launch_synthetic_x(x0, a, b, n, kind, c1, c2, s, static_cast<__nv_bfloat16*>(out),
@@ -379,6 +399,7 @@ int fo_synthetic_x(const float* x0, const float* a, const float* b, size_t n, in
 
 int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads, int head_dim,
                   int rows, int order_d, const uint8_t* select, void* stream) {
+  FO_RANGE();
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (rows != ceil_div_d(seq, kTile)) return fail(FO_ERR_SHAPE, "rows != ceil(seq/128)");
@@ -390,6 +411,7 @@ int fo_cache_push(const void* o, void* cache, int32_t* valid, int seq, int heads
 
 int fo_cache_push_tile(const void* tile, void* cache, int32_t* valid, int seq, int heads,
                        int head_dim, int rows, int order_d, int head, int block, void* stream) {
+  FO_RANGE();
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (!tile || !cache || !valid) return fail(FO_ERR_PARAM, "cache_push_tile: null pointer");
@@ -408,6 +430,7 @@ int fo_cache_push_tile(const void* tile, void* cache, int32_t* valid, int seq, i
 int fo_gemm_q(const void* x, int seq, int d_model, const void* w_qt, int heads, int head_dim,
               const float* norm_w, const float* rope_cos, const float* rope_sin, float eps,
               const void* plan_ws, int dense, void* q_out, void* stream) {
+  FO_RANGE();
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (d_model % 64 != 0 || d_model < 64) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 64");
@@ -450,6 +473,7 @@ int fo_gemm_qkv(const void* x, int seq, int d_model, const void* w_qkvt, int hea
                 const float* q_norm, const float* k_norm, const float* rope_cos,
                 const float* rope_sin, float eps, const void* plan_ws, int dense, void* q_out,
                 void* k_out, void* v_out, void* stream) {
+  FO_RANGE();
   int rc = check_head_dim(head_dim);
   if (rc) return rc;
   if (d_model % 64 != 0 || d_model < 64) return fail(FO_ERR_SHAPE, "d_model must be a multiple of 64");
@@ -528,6 +552,7 @@ static int gemm_o_common(const void* o, const void* cache, const void* w_outt, i
 int fo_gemm_o_update(const void* o, const void* cache, const void* w_outt, int seq, int heads,
                      int head_dim, int d_model, int order_d, const void* plan_ws, void* out,
                      void* bias, uint32_t* status, void* stream) {
+  FO_RANGE();
   GemmOParams p;
   CUtensorMap am, cm, wm;
   int rc = gemm_o_common(o, cache, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p, am,
@@ -567,6 +592,7 @@ int fo_gemm_o_dispatch_rows(const void* o, const void* w_outt, const void* bias,
                             const int32_t* orders, int seq, int heads, int head_dim, int d_model,
                             int order_d, const float* coef, const void* plan_ws, int block_begin,
                             int block_end, int max_sms, void* out, void* stream) {
+  FO_RANGE();
   GemmOParams p;
   CUtensorMap am, cm, wm;
   int rc = gemm_o_common(o, nullptr, w_outt, seq, heads, head_dim, d_model, order_d, plan_ws, p,
@@ -603,6 +629,7 @@ int fo_gemm_o_dispatch_rows(const void* o, const void* w_outt, const void* bias,
 
 int fo_check_active_match(const uint8_t* s_c_a, const uint8_t* s_c_b, int heads, int rows,
                           int pool_n, uint32_t* status, void* stream) {
+  FO_RANGE();
   int rc = check_symbol_dims(heads, rows, 1, pool_n);
   if (rc) return rc;
   const int total = heads * rows;
@@ -621,6 +648,7 @@ size_t fo_policy_workspace_bytes(int seq, int heads, int pool_n) {
 int fo_generate_masks(const void* q, const void* k, int seq, int heads, int n_text, int pool_n,
                       double tau_q, double tau_kv, double s_q, int guard, uint8_t* cache_bits,
                       uint8_t* skip_bits, void* workspace, size_t workspace_bytes, void* stream) {
+  FO_RANGE();
   if (!q || !k || !cache_bits || !skip_bits || !workspace)
     return fail(FO_ERR_PARAM, "generate_masks: null pointer");
   if (seq <= 0 || heads <= 0) return fail(FO_ERR_SHAPE, "generate_masks: seq=%d heads=%d", seq, heads);
@@ -661,6 +689,7 @@ size_t fo_policy_map_workspace_bytes(int seq_q, int seq_k, int heads, int pool_q
 int fo_policy_compressed_map(const void* q, const void* k, int is_f32, int seq_q, int seq_k,
                              int heads, int head_dim, int pool_q, int pool_k, float* p_tilde,
                              void* workspace, size_t workspace_bytes, void* stream) {
+  FO_RANGE();
   if (!q || !k || !p_tilde || !workspace) return fail(FO_ERR_PARAM, "compressed_map: null pointer");
   if (seq_q <= 0 || seq_k <= 0 || heads <= 0)
     return fail(FO_ERR_SHAPE, "compressed_map: seq=%d/%d heads=%d", seq_q, seq_k, heads);
@@ -685,6 +714,7 @@ int fo_policy_compressed_map(const void* q, const void* k, int is_f32, int seq_q
 
 int fo_policy_block_scores(const float* p_tilde, int heads, int rows, int cols, int n_t,
                            double* contribution, double* guidance, void* stream) {
+  FO_RANGE();
   if (!p_tilde || !contribution || !guidance) return fail(FO_ERR_PARAM, "block_scores: null pointer");
   if (heads <= 0 || rows <= 0 || cols <= 0 || rows > kPolicyMaxBlocks || cols > kPolicyMaxBlocks)
     return fail(FO_ERR_SHAPE, "block_scores: %d x %d map", rows, cols);
@@ -698,6 +728,7 @@ int fo_policy_block_scores(const float* p_tilde, int heads, int rows, int cols, 
 
 int fo_policy_select_cached(const double* contribution, const double* guidance, int heads, int n,
                             double tau_q, uint8_t* cached, void* stream) {
+  FO_RANGE();
   if (!contribution || !guidance || !cached) return fail(FO_ERR_PARAM, "select_cached: null pointer");
   if (heads <= 0 || n < 0 || n > kPolicyMaxBlocks) return fail(FO_ERR_SHAPE, "select_cached: n=%d", n);
   if (!(tau_q >= 0.0 && tau_q <= 1.0)) return fail(FO_ERR_PARAM, "tau_q must be in [0, 1], got %g", tau_q);
@@ -710,6 +741,7 @@ int fo_policy_select_cached(const double* contribution, const double* guidance, 
 
 int fo_policy_select_skip(const float* p_tilde, const uint8_t* compute, int heads, int rows,
                           int cols, int n_t, double tau_kv, int guard, uint8_t* keep, void* stream) {
+  FO_RANGE();
   if (!p_tilde || !compute || !keep) return fail(FO_ERR_PARAM, "select_skip: null pointer");
   if (heads <= 0 || rows <= 0 || cols <= 0 || rows > kPolicyMaxBlocks || cols > kPolicyMaxBlocks)
     return fail(FO_ERR_SHAPE, "select_skip: %d x %d map", rows, cols);

@@ -14,6 +14,7 @@ cached bias) are summed by one all-reduce — exact by linearity of the
 projection and the forecast.
 """
 
+import functools
 import os
 from dataclasses import dataclass
 
@@ -98,6 +99,22 @@ def _allreduce(out, group):
     return out
 
 
+def _nvtx(name):
+    """An NVTX range around a layer step (the C-ABI entry points inside carry
+    their own ranges), for nsys / ncu --nvtx filtering."""
+    def wrap(fn):
+        @functools.wraps(fn)
+        def ranged(*args, **kwargs):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return ranged
+    return wrap
+
+
+@_nvtx("fo.update_step")
 def update_step(state, x, symbols_next, order_d, *, group=None, check=True, policy=None, t=0):
     """Refresh symbols, cache and bias; compute the step densely
     (pipeline.py:244-288). The next window's symbols come from `policy`
@@ -167,6 +184,7 @@ def _dispatch_out_allreduce(o, p, state, elapsed_k, interval_n, order_d, out, gr
     return out
 
 
+@_nvtx("fo.dispatch_step")
 def dispatch_step(state, x, elapsed_k, interval_n, order_d, *, group=None, check=True, fill=None,
                   bufs=None, chunks=1, comm_sms=0):
     """Sparse execution against the governing symbols (pipeline.py:291-326).
