@@ -162,6 +162,7 @@ struct ItemCursor {
 #ifdef FO_CS_TIMING  // tools/cs_timing.py: per-CTA start/end (globaltimer), SM id, tiles
 __device__ unsigned long long g_cs_timing[16 * 1024];
 __device__ long long g_cs_ph[5 * 1024];
+__device__ long long g_cs_ep[6 * 1024];  // epilogue sub-phases (cycles, summed over items)
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -510,6 +511,8 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
     unsigned long long t_mark = 0, g_a = 0, g_b = 0, g_c = 0, n_it = 0;
     long long g_sw = 0, g_sb = 0, g_st = 0;  // steady-state tiles: S wait, softmax busy (cycles)
     long long g_ph[5] = {0, 0, 0, 0, 0};      // softmax phases (cycles)
+    long long g_ep[6] = {0, 0, 0, 0, 0, 0};   // epilogue sub-phases (cycles)
+    long long te_prev = 0;
 #endif
     for (int k = 0; have; ++k, ++qi) {
       const int2 it = it_cur;
@@ -703,6 +706,17 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 #endif
       o_base += n - 1;  // o_done phases of this item
       tc_fence_after();
+#ifdef FO_CS_TIMING
+      te_prev = clock64();
+      auto ep_mark = [&](int k) {
+        const long long t = clock64();
+        if (tmr) g_ep[k] += t - te_prev;
+        te_prev = t;
+      };
+#define FO_EP_MARK(k) ep_mark(k)
+#else
+#define FO_EP_MARK(k) ((void)0)
+#endif
       float l_row;
       if (FO_CS_TC_ROWSUM) {
         uint32_t lsum[16];
@@ -717,6 +731,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         l_row = bars->xsum[0][r] + bars->xsum[1][r];
       }
       const float inv_l = 1.f / l_row;
+      FO_EP_MARK(0);  // l from TMEM
       const int ib = i + rank;  // this CTA's query block (a pair's missing partner: ib == t_q)
       const int row = ib * kTile + r;
       const bool row_ok = row < p.S;
@@ -737,6 +752,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
                     static_cast<unsigned long long>(n));
         if (p.cache && p.valid) p.valid[(size_t)h * p.t_q + ib] = vn;
       }
+      FO_EP_MARK(1);  // next item's record, counters
       const uint32_t oa = tbase + lane_off + TM_O + col0;
 #if FO_CS_TMA_OUT
       // this warp's staging box: rows q4*32.., its columns; chunk q of row r at
@@ -751,6 +767,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
         tmem_ld32(oa + c * 32, o);
         tmem_ld_wait();
         reg_fence_cs(o);
+        FO_EP_MARK(2 + 2 * c);  // O chunk from TMEM (c = 0: marks 2, c = 1: marks 4)
         float of[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) of[k] = __uint_as_float(o[k]) * inv_l;
@@ -834,8 +851,11 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
           }
         }
       }
+      FO_EP_MARK(3);  // the last chunk's scale, pack, stage, TMA store (chunk 0's land in 3 too)
       tc_fence_before();
       mbar_arrive(&bars->o_free);
+      FO_EP_MARK(5);
+#undef FO_EP_MARK
 #ifdef FO_CS_TIMING
       if (tmr) {
         const unsigned long long t = global_ns();
@@ -854,6 +874,7 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
       g_cs_timing[16 * blockIdx.x + 13] = g_sb;
       g_cs_timing[16 * blockIdx.x + 14] = g_st;
       for (int k = 0; k < 5; ++k) g_cs_ph[5 * blockIdx.x + k] = g_ph[k];
+      for (int k = 0; k < 6; ++k) g_cs_ep[6 * blockIdx.x + k] = g_ep[k];
     }
 #endif
 #if FO_CS_TMA_OUT
@@ -879,6 +900,9 @@ __global__ void __launch_bounds__(attn_cs::NTHREADS, 1)
 extern "C" __attribute__((visibility("default"))) int fo_debug_cs_timing(unsigned long long* out,
                                                                        int n) {
   return (int)cudaMemcpyFromSymbol(out, g_cs_timing, sizeof(unsigned long long) * 16 * n);
+}
+extern "C" __attribute__((visibility("default"))) int fo_debug_cs_epilogue(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cs_ep, sizeof(long long) * 6 * n);
 }
 extern "C" __attribute__((visibility("default"))) int fo_debug_cs_phases(long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, g_cs_ph, sizeof(long long) * 5 * n);

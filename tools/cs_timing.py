@@ -66,3 +66,9 @@ if hasattr(lib, "fo_debug_cs_phases") and lib.fo_debug_cs_phases(ph, 1024) == 0:
     names = ["S tmem->reg", "max+exchange", "exp+pack", "P reg->tmem", "check+arrive"]
     print("softmax phases (cycles/tile): " + ", ".join(f"{k} {v:.0f}" for k, v in zip(names, P.mean(0))))
 
+ep = (ctypes.c_longlong * (6 * 1024))()
+if hasattr(lib, "fo_debug_cs_epilogue") and lib.fo_debug_cs_epilogue(ep, 1024) == 0:
+    E = np.array(ep[:6 * n], dtype=np.int64).reshape(n, 6) / nit[:, None]
+    names = ["l from TMEM", "next record+counters", "O chunk0 TMEM ld", "chunk1 scale/stage/TMA store",
+             "chunk0 scale/stage/TMA store + chunk1 TMEM ld", "fence+arrive o_free"]
+    print("epilogue (cycles/item): " + ", ".join(f"{k} {v:.0f}" for k, v in zip(names, E.mean(0))))
