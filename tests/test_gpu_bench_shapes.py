@@ -367,3 +367,37 @@ def test_fused_qkv_projection_matches_separate_launches():
             rows = torch.from_numpy(np.repeat(active.T, T, axis=0)[:S]).cuda()
             assert torch.isnan(q[~rows]).all()  # skipped tiles keep the fill
         assert torch.equal(q[rows], q0[rows])
+
+
+@pytest.mark.parametrize("S,H,dm", [(1000, 3, 256), (777, 5, 384), (128, 1, 128)])
+def test_fused_qkv_ragged_and_odd_heads(S, H, dm):
+    """The fused projection at a ragged last block (rows past S clipped), odd
+    head counts (the last head alone: N = 128 jobs in every segment) and one
+    block: still equal to the separate launches bit for bit."""
+    import torch
+
+    m = fo()
+    rng = np.random.default_rng(S + H)
+    T = 128
+    t = -(-S // T)
+    g = torch.Generator(device="cuda").manual_seed(S)
+    x = torch.randn(S, dm, device="cuda", generator=g).bfloat16()
+    w = [torch.randn(H, dm, T, device="cuda", generator=g) * dm ** -0.5 for _ in range(3)]
+    qn = 1 + 0.05 * torch.randn(H, T, device="cuda", generator=g)
+    kn = 1 + 0.05 * torch.randn(H, T, device="cuda", generator=g)
+    params = m.LayerParams.from_reference(w[0], w[1], w[2], qn, kn,
+                                          torch.randn(H, T, dm, device="cuda") * T ** -0.5)
+    active = rng.random((H, t)) >= 0.5
+    active[:, 0] = True
+    sym = m.encode_symbols(active, np.ones((H, t, t), bool), 1)
+    for phase, sy in (("dispatch", sym), ("update", None)):
+        q, k, v = m.project_qkv(x, params.w_qkv, qn, kn, sy, phase, fill=float("nan"))
+        q0 = m.project_q(x, params.w_q, qn, sy, phase, fill=float("nan"))
+        k0, v0 = m.project_kv(x, params)
+        torch.cuda.synchronize()
+        assert torch.equal(k, k0) and torch.equal(v, v0)
+        rows = torch.ones(S, H, dtype=torch.bool, device="cuda")
+        if phase == "dispatch":
+            rows = torch.from_numpy(np.repeat(active.T, T, axis=0)[:S]).cuda()
+        assert torch.equal(q[rows], q0[rows])
+        assert torch.isfinite(k).all() and torch.isfinite(v).all()
