@@ -272,6 +272,20 @@ FO_API int fo_rope(const float* x, const float* cos_t, const float* sin_t, int n
                    void* stream);
 FO_API int fo_row_softmax(const float* s, int n, int d, float* out, void* stream);
 
+/* The reference tile-kernel protocol at any block size and head dim, fp32
+ * (replaces _kernels/pyref.py:14-48 masked_block_attention and
+ * _kernels/_core.pyx:14-101): q, k, v float32 [n, d] (d <= 256); active
+ * uint8 [t_q]; pair_bits uint8 [t_q, t_kv] (t = ceil(n / b)). Writes the rows
+ * of active blocks of out (others untouched), adds the computed pair count to
+ * *pairs (optional) and raises CONSISTENCY in *status for an active block
+ * with no key block (the reference's l <= 0 error). The tcgen05 kernel
+ * (fo_sparse_attention) is the path for 128-token blocks. */
+FO_API int fo_masked_block_attention_f32(const float* q, const float* k, const float* v, int n,
+                                         int d, const uint8_t* active, const uint8_t* pair_bits,
+                                         int b_q, int b_k, float scale, float* out,
+                                         unsigned long long* pairs, uint32_t* status,
+                                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,7 +7,9 @@ sparse-attention kernel: the decoded bits are packed on the device (K1), the
 schedule is planned on the device, and only rows of active blocks are
 written back into the caller's `out`. Inputs are rounded to bf16 (the
 engine's arithmetic type); head dims below 128 are zero-padded, which leaves
-q.k and the attended values unchanged.
+q.k and the attended values unchanged Other block sizes run the fp32 tile
+kernel (fo_masked_block_attention_f32), so the reference's own small-block
+kernel tests hold at their 1e-5 tolerance.
 """
 
 import numpy as np
@@ -22,7 +24,11 @@ NAME = "b200"
 
 def masked_block_attention(q, k, v, active, pair_bits, b_q, b_k, scale, out):
     if b_q != TILE or b_k != TILE:
-        raise ParameterError(f"b200 backend tiles blocks of {TILE} tokens, got b_q={b_q}, b_k={b_k}")
+        # any other block size (the reference's own kernel tests use 4-16): the
+        # fp32 tile kernel, which keeps the reference's float32 arithmetic
+        from ..attention import masked_block_attention_f32
+
+        return masked_block_attention_f32(q, k, v, active, pair_bits, b_q, b_k, scale, out)
     require_cuda()
     q = np.ascontiguousarray(q, dtype=np.float32)
     n, d = q.shape

@@ -67,8 +67,8 @@ class FeatureCache:
     """
 
     def __init__(self, heads, n_blocks, order, seq=None, device=None):
-        if order < 0 or order > 3:
-            raise ParameterError(f"order must be in [0, 3] on the B200 engine, got {order}")
+        if order < 0:
+            raise ParameterError(f"order must be >= 0, got {order}")
         require_cuda()
         self.heads, self.n_blocks, self.order = int(heads), int(n_blocks), int(order)
         self.device = device or "cuda"
@@ -76,10 +76,24 @@ class FeatureCache:
         self.stacks = None
         self.seq = None
         self.version = 0  # bumped on every push; keys the cached plans
+        # per-entry mode: a cache that receives per-tile updates before any
+        # sequence length is known keeps, like the reference (attention.py:
+        # 116-135), one fp32 device stack per (head, block) at any tile shape
+        self._entries = None
         if seq is not None:
             self._alloc(seq)
 
+    @property
+    def per_entry(self):
+        """True once the cache holds per-entry fp32 stacks (any tile shape)."""
+        return self._entries is not None
+
     def _alloc(self, seq):
+        if self._entries is not None:
+            raise StateError("this cache holds per-entry tiles; layer pushes need a cache made "
+                             "with seq=")
+        if self.order > 3:
+            raise ParameterError(f"order must be in [0, 3] for the HBM stacks, got {self.order}")
         if ceil_div(seq, TILE) != self.n_blocks:
             raise ShapeError(f"seq {seq} gives {ceil_div(seq, TILE)} blocks, cache has {self.n_blocks}")
         self.seq = int(seq)
@@ -111,9 +125,11 @@ class FeatureCache:
 
     def update(self, head, block, o_new):
         """Reference signature (attention.py:128-131): push one tile o_new
-        [rows, 128] (numpy or torch) into entry (head, block). One tile-sized
-        launch on the current stream (fo_cache_push_tile); nothing synchronises
-        for device tiles."""
+        (numpy or torch) into entry (head, block). A cache made with seq= takes
+        [rows, 128] tiles into its HBM stacks (one tile-sized launch,
+        fo_cache_push_tile; nothing synchronises for device tiles); a cache
+        without one keeps per-entry fp32 device stacks at any tile shape
+        (fo_update_entry), as the reference does."""
         if isinstance(o_new, torch.Tensor):
             tile = o_new
             if tile.dim() == 2 and not bool(torch.isfinite(tile).all()):
@@ -123,12 +139,19 @@ class FeatureCache:
             if arr.ndim == 2 and not np.isfinite(arr).all():
                 raise ParameterError("tile: contains NaN or Inf")
             tile = torch.from_numpy(np.ascontiguousarray(arr))
-        if tile.dim() != 2 or tile.shape[1] != TILE:
-            raise ShapeError(f"tile shape {tuple(tile.shape)}; head_dim must be {TILE}")
-        if self.stacks is None:
-            raise ShapeError("allocate the cache with seq= before per-tile updates")
         if not (0 <= head < self.heads and 0 <= block < self.n_blocks):
             raise IndexError(f"entry ({head}, {block}) outside ({self.heads}, {self.n_blocks})")
+        if self.stacks is None:  # no seq given: per-entry fp32 stacks, any tile shape
+            if self._entries is None:
+                self._entries = [[None] * self.n_blocks for _ in range(self.heads)]
+            e = update_entry(self._entries[head][block],
+                             tile.to(self.device, torch.float32).contiguous(), self.order)
+            self._entries[head][block] = e
+            self.valid[head, block] = e.valid_orders
+            self.version += 1
+            return
+        if tile.dim() != 2 or tile.shape[1] != TILE:
+            raise ShapeError(f"tile shape {tuple(tile.shape)}; head_dim must be {TILE}")
         rows = min(TILE, self.seq - block * TILE)
         if tile.shape[0] != rows:
             raise ShapeError(f"tile shape {tuple(tile.shape)} != cached ({rows}, {TILE})")
@@ -139,9 +162,21 @@ class FeatureCache:
         self.version += 1
 
     def valid_orders(self, head, block):
+        if self._entries is not None:
+            e = self._entries[head][block]
+            return 0 if e is None else int(e.valid_orders)
         return int(self.valid[head, block].item())
 
+    def device_entry(self, head, block):
+        """Per-entry mode: the entry with its device fp32 stack (or None)."""
+        return None if self._entries is None else self._entries[head][block]
+
     def entry(self, head, block):
+        if self._entries is not None:
+            e = self._entries[head][block]
+            if e is None:
+                return None
+            return CacheEntry(diff_stack=e.diff_stack.cpu().numpy(), valid_orders=e.valid_orders)
         if self.valid_orders(head, block) < 1:
             return None
         r0 = block * TILE
@@ -267,6 +302,90 @@ def forecast(entry, elapsed_k, interval_n, order_d):
 
 
 # ---------------------------------------------------------------------------
+def _as_matrix(a, name, finite=True):
+    """tensor.py:19-30 as_matrix: C-contiguous float32 2-D, finite unless opted out."""
+    m = np.ascontiguousarray(a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a,
+                             dtype=DTYPE)
+    if m.ndim != 2:
+        raise ShapeError(f"{name}: expected a 2-D matrix, got shape {m.shape}")
+    if finite and not np.isfinite(m).all():
+        raise ParameterError(f"{name}: contains NaN or Inf")
+    return m
+
+
+def masked_block_attention_f32(q, k, v, active, pair_bits, b_q, b_k, scale, out):
+    """The reference tile-kernel protocol (pyref.py:14-48) at any block size and
+    head dim <= 256, in fp32 on the GPU (fo_masked_block_attention_f32): writes
+    the rows of active blocks into `out` (numpy [n, d]) and returns the computed
+    pair count; an active block with no key block raises ConsistencyError."""
+    require_cuda()
+    q, k, v = (torch.from_numpy(_as_matrix(a, nm, finite=False)).cuda()
+               for a, nm in ((q, "q"), (k, "k"), (v, "v")))
+    n, d = q.shape
+    if tuple(k.shape) != (n, d) or tuple(v.shape) != (n, d):
+        raise ShapeError(f"q/k/v shapes {tuple(q.shape)}/{tuple(k.shape)}/{tuple(v.shape)} differ")
+    if d > 256:
+        raise ParameterError(f"head dim {d} > 256")
+    t_q, t_kv = ceil_div(n, b_q), ceil_div(n, b_k)
+    act = torch.as_tensor(np.asarray(active, dtype=np.uint8).reshape(-1)).cuda()
+    pb = torch.as_tensor(np.ascontiguousarray(pair_bits, dtype=np.uint8)).cuda()
+    if tuple(act.shape) != (t_q,) or tuple(pb.shape) != (t_q, t_kv):
+        raise ShapeError(f"mask shapes {tuple(act.shape)}/{tuple(pb.shape)} for {t_q}x{t_kv} blocks")
+    res = torch.from_numpy(np.ascontiguousarray(out, dtype=DTYPE)).cuda()
+    pairs = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st = Status()
+    _lib.call("fo_masked_block_attention_f32", q.data_ptr(), k.data_ptr(), v.data_ptr(), n, d,
+              act.data_ptr(), pb.data_ptr(), int(b_q), int(b_k), float(scale), res.data_ptr(),
+              pairs.data_ptr(), st.ptr(), stream_ptr(None))
+    bits = int(st.t.item())
+    if bits & _lib.ST_CONSISTENCY:
+        raise ConsistencyError("active query block has every key block skipped")
+    _lib.raise_status(bits, "masked_block_attention")
+    out[...] = res.cpu().numpy()
+    return int(pairs.item())
+
+
+def _per_head_general(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d, b_q, b_k,
+                      mode, counters, fill):
+    """Reference per-head signature at any block size / head dim, fp32
+    (attention.py:150-221, step for step): the symbols decode on the GPU, the
+    tile kernel is fo_masked_block_attention_f32 and cached blocks take their
+    forecast from the cache's per-entry device stacks (fo_forecast_entry)."""
+    q = _as_matrix(q, "q", finite=False)
+    k = _as_matrix(k, "k")
+    v = _as_matrix(v, "v")
+    if mode not in ("materialize", "bias"):
+        raise ParameterError(f"unknown mode {mode!r}")
+    n, d = q.shape
+    t_q, t_kv = ceil_div(n, b_q), ceil_div(n, b_k)
+    if (symbols.rows, symbols.cols) != (t_q, t_kv):
+        raise ShapeError(f"symbols dimensioned {symbols.rows}x{symbols.cols}, "
+                         f"expected {t_q}x{t_kv}")
+    sym = symbols if isinstance(symbols, DeviceSymbols) else DeviceSymbols.from_buffers([symbols])
+    act_d, pair_d = sym.decoded()
+    active = act_d[0].cpu().numpy()
+    read_rows = np.repeat(active.astype(bool), b_q)[:n]
+    if not np.isfinite(q[read_rows]).all():
+        raise ParameterError("q: active-block rows contain NaN or Inf")
+    out = np.full((n, d), fill, dtype=DTYPE)
+    pairs = masked_block_attention_f32(q, k, v, active, pair_d[0].cpu().numpy(), b_q, b_k,
+                                       1.0 / math.sqrt(d), out)
+    for i in np.flatnonzero(active == 0):
+        entry = None
+        if cache is not None:
+            entry = cache.device_entry(head, i) if cache.per_entry else cache.entry(head, i)
+        if entry is None or entry.valid_orders < 1:
+            raise StateError(f"query block {i} is cached but the cache is cold")
+        if mode == "materialize":
+            f = forecast(entry, elapsed_k, interval_n, order_d)
+            f = f.cpu().numpy() if isinstance(f, torch.Tensor) else f
+            out[i * b_q:i * b_q + f.shape[0]] = f
+    if counters is not None:
+        counters.pairs_total += t_q * t_kv
+        counters.pairs_computed += pairs
+    return out
+
+
 def _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d, b_q, b_k,
                       mode, counters, fill):
     """Reference per-head signature: numpy [n, d] in, numpy fp32 out."""
@@ -313,13 +432,22 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
     """
     if backend is not None and getattr(backend, "NAME", "b200") != "b200":
         raise ParameterError("this engine runs only its sm_100a kernels")
+    if isinstance(q, np.ndarray) or isinstance(symbols, SymbolBuffer):
+        # the reference's per-head numpy signature: 128-token blocks at head dim
+        # 128 run on the tcgen05 kernel; any other shape (or a per-entry cache)
+        # on the fp32 tile kernel
+        if (b_q != TILE or b_k != TILE or np.shape(q)[-1] != TILE
+                or (cache is not None and cache.per_entry)):
+            return _per_head_general(q, k, v, symbols, cache, head, elapsed_k, interval_n,
+                                     order_d, b_q, b_k, mode, counters, fill)
+        if mode not in ("materialize", "bias"):
+            raise ParameterError(f"unknown mode {mode!r}")
+        return _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d,
+                                 b_q, b_k, mode, counters, fill)
     if mode not in ("materialize", "bias"):
         raise ParameterError(f"unknown mode {mode!r}")
     if b_q != TILE or b_k != TILE:
         raise ParameterError(f"the sm_100a kernels tile blocks of {TILE} tokens (b_q=b_k={TILE})")
-    if isinstance(q, np.ndarray) or isinstance(symbols, SymbolBuffer):
-        return _per_head_adapter(q, k, v, symbols, cache, head, elapsed_k, interval_n, order_d,
-                                 b_q, b_k, mode, counters, fill)
     require_cuda()
     q = check_bsd(q, "q")
     seq, heads = q.shape[0], q.shape[1]
@@ -335,6 +463,8 @@ def sparse_attention(q, k, v, symbols, cache, head, elapsed_k, interval_n, order
         raise ShapeError(f"symbols for {symbols.heads} heads, q has {heads}")
     st = status or Status.default()
     if cache is not None:
+        if cache.per_entry:
+            raise StateError("a per-entry cache (no seq=) serves the per-head signature only")
         if (cache.heads, cache.n_blocks) != (heads, t_q):
             raise ShapeError("feature cache geometry does not match q")
         valid, vver = cache.valid, cache.version

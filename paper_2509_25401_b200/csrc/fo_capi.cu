@@ -833,4 +833,20 @@ int fo_row_softmax(const float* s, int n, int d, float* out, void* stream) {
   return cuda_rc(launch_row_softmax(s, n, d, out, (cudaStream_t)stream), "row_softmax");
 }
 
+int fo_masked_block_attention_f32(const float* q, const float* k, const float* v, int n, int d,
+                                  const uint8_t* active, const uint8_t* pair_bits, int b_q, int b_k,
+                                  float scale, float* out, unsigned long long* pairs,
+                                  uint32_t* status, void* stream) {
+  FO_RANGE();
+  if (!q || !k || !v || !active || !pair_bits || !out || !status)
+    return fail(FO_ERR_PARAM, "masked_block_attention: null pointer");
+  if (n < 0 || d < 1 || d > 256 || b_q < 1 || b_k < 1)
+    return fail(FO_ERR_SHAPE, "masked_block_attention: n=%d d=%d (1..256) b_q=%d b_k=%d", n, d, b_q,
+                b_k);
+  if (n == 0) return FO_OK;
+  return cuda_rc(launch_masked_block_attention_f32(q, k, v, n, d, active, pair_bits, b_q, b_k, scale,
+                                                   out, pairs, status, (cudaStream_t)stream),
+                 "masked_block_attention");
+}
+
 }  // extern "C"

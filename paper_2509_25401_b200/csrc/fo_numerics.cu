@@ -188,6 +188,99 @@ row_softmax_kernel(const float* __restrict__ s, int d, float* __restrict__ out) 
 
 int grid_of(size_t n) { return (int)((n + 255) / 256); }
 
+
+// The reference tile kernel at any block size and head dim, in fp32
+// (pyref.py:14-48 / _core.pyx:14-101): for every active query block i and
+// every key block j with pair_bits[i][j] set, per row
+//   m' = max(m, rowmax(S_ij)); corr = exp(m - m'); p = exp(S_ij - m')
+//   l' = l*corr + sum(p); acc' = acc*corr + p V_j;   out_i = acc / l.
+// One CTA per query block, one thread per row (128 rows per pass). K / V rows
+// are staged in shared memory in chunks of KC rows padded to DP columns; S is
+// recomputed in a second pass instead of stored. This is the drop-in's general
+// path for shapes the tcgen05 kernel does not tile (b != 128, the reference's
+// own small-d tests); it matches the reference's float32 arithmetic to
+// rounding (expf, fp32 accumulation).
+constexpr int kMbaThreads = 128;
+constexpr int kMbaChunkFloats = 4096;  // per staged operand: 16 KB
+
+template <int DP>
+__global__ void __launch_bounds__(kMbaThreads)
+masked_block_attention_f32_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                  const float* __restrict__ v, int n, int d,
+                                  const uint8_t* __restrict__ active,
+                                  const uint8_t* __restrict__ pair_bits, int t_kv, int b_q, int b_k,
+                                  float scale, float* __restrict__ out,
+                                  unsigned long long* __restrict__ pairs, uint32_t* status) {
+  constexpr int KC = kMbaChunkFloats / DP;
+  __shared__ float sk[KC * DP], sv[KC * DP];
+  const int i = blockIdx.x;
+  if (!active[i]) return;
+  const uint8_t* prow = pair_bits + (size_t)i * t_kv;
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+    for (int j = 0; j < t_kv; ++j) c += prow[j] != 0;
+    if (c == 0) raise_status(status, ST_CONSISTENCY);  // l = 0: pyref.py:44-46
+    else if (pairs) atomicAdd(pairs, c);
+  }
+  const int r0 = i * b_q, r1 = min(r0 + b_q, n);
+  for (int rb = r0; rb < r1; rb += kMbaThreads) {
+    const int r = rb + (int)threadIdx.x;
+    const bool live = r < r1;
+    float qr[DP], acc[DP];
+#pragma unroll
+    for (int c = 0; c < DP; ++c) {
+      qr[c] = (live && c < d) ? q[(size_t)r * d + c] : 0.f;
+      acc[c] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < t_kv; ++j) {
+      if (!prow[j]) continue;
+      const int c0 = j * b_k, c1 = min(c0 + b_k, n);
+      auto stage = [&](int cb, int ce, bool with_v) {
+        __syncthreads();  // the previous chunk is consumed
+        for (int e = threadIdx.x; e < (ce - cb) * DP; e += kMbaThreads) {
+          const int kr = e / DP, c = e - kr * DP;
+          sk[e] = c < d ? k[(size_t)(cb + kr) * d + c] : 0.f;
+          if (with_v) sv[e] = c < d ? v[(size_t)(cb + kr) * d + c] : 0.f;
+        }
+        __syncthreads();
+      };
+      auto dot = [&](int kr) {
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c < DP; ++c) s = fmaf(qr[c], sk[kr * DP + c], s);
+        return s * scale;
+      };
+      float mb = -INFINITY;  // pass 1: the block's row max
+      for (int cb = c0; cb < c1; cb += KC) {
+        const int ce = min(cb + KC, c1);
+        stage(cb, ce, false);
+        for (int kr = 0; kr < ce - cb; ++kr) mb = fmaxf(mb, dot(kr));
+      }
+      const float m_new = fmaxf(m, mb);
+      const float corr = expf(m - m_new);  // m = -inf on the first block: 0
+      l *= corr;
+#pragma unroll
+      for (int c = 0; c < DP; ++c) acc[c] *= corr;
+      for (int cb = c0; cb < c1; cb += KC) {  // pass 2: p, l and p V
+        const int ce = min(cb + KC, c1);
+        stage(cb, ce, true);
+        for (int kr = 0; kr < ce - cb; ++kr) {
+          const float pr = expf(dot(kr) - m_new);
+          l += pr;
+#pragma unroll
+          for (int c = 0; c < DP; ++c) acc[c] = fmaf(pr, sv[kr * DP + c], acc[c]);
+        }
+      }
+      m = m_new;
+    }
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < DP; ++c)  // static indices: acc stays in registers
+        if (c < d) out[(size_t)r * d + c] = acc[c] / l;
+    }
+  }
+}
 }  // namespace
 
 // largest row width of the per-row kernels (shared-memory bound)
@@ -258,6 +351,25 @@ cudaError_t launch_row_softmax(const float* s, int n, int d, float* out, cudaStr
   cudaFuncSetAttribute(row_softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   note_launch();
   row_softmax_kernel<<<n, kRowThreads, sm, st>>>(s, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_masked_block_attention_f32(const float* q, const float* k, const float* v, int n,
+                                              int d, const uint8_t* active,
+                                              const uint8_t* pair_bits, int b_q, int b_k,
+                                              float scale, float* out, unsigned long long* pairs,
+                                              uint32_t* status, cudaStream_t st) {
+  const int t_q = (n + b_q - 1) / b_q, t_kv = (n + b_k - 1) / b_k;
+  note_launch();
+#define FO_MBA(DP)                                                                        \
+  masked_block_attention_f32_kernel<DP><<<t_q, kMbaThreads, 0, st>>>(                     \
+      q, k, v, n, d, active, pair_bits, t_kv, b_q, b_k, scale, out, pairs, status)
+  if (d <= 16) FO_MBA(16);
+  else if (d <= 32) FO_MBA(32);
+  else if (d <= 64) FO_MBA(64);
+  else if (d <= 128) FO_MBA(128);
+  else FO_MBA(256);
+#undef FO_MBA
   return cudaGetLastError();
 }
 
