@@ -404,10 +404,10 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
   // in one round draw a light one in the next
   auto job_of = [&](int rr) { return rr * ncl + ((rr & 1) ? ncl - 1 - cid : cid); };
   const int nkb = p.dm / BK;
-  // job -> this CTA's block i, head h and width (n256: heads h, h+1); false: no
-  // block for this CTA (it loads zero rows past the end and skips its epilogue)
-  // seg: 0 Q, 1 K, 2 V (rows seg*H*128.. of the fused weight)
-  auto job = [&](int c, int& i, int& h, bool& n256, int& seg) -> bool {
+  // job -> this CTA's block i, head h and width (n256: heads h, h2 as one N=256
+  // tile); false: no block for this CTA (it loads zero rows past the end and
+  // skips its epilogue). seg: 0 Q, 1 K, 2 V (rows seg*H*128.. of the fused weight)
+  auto job = [&](int c, int& i, int& h, int& h2, bool& n256, int& seg) -> bool {
     int i0, i1;
     seg = 0;
     if (c < n_kv) {  // fused K / V: block-pair-major, then K / V, then head pair
@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       i1 = 2 * bp + 1 < p.t_q ? 2 * bp + 1 : -1;
       h = 2 * r;
       n256 = r < nph;
+      h2 = h + 1;
     } else if (p.dense) {  // block-pair-major
       c -= n_kv;
       const int bp = c / npj, r = c - bp * npj;
@@ -424,12 +425,14 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
       i1 = 2 * bp + 1 < p.t_q ? 2 * bp + 1 : -1;
       h = 2 * r;
       n256 = r < nph;
+      h2 = h + 1;
     } else {
       const int2 code = p.jobs[c - n_kv];
       i0 = code.x & 0xFFFF;
       i1 = (code.x >> 16) - 1;
       h = code.y & 0xFF;
       n256 = (code.y >> 8) & 1;
+      h2 = (code.y >> 16) & 0xFF;  // any head (heads paired per block by the plan)
     }
     i = rank ? (i1 >= 0 ? i1 : p.t_q) : i0;
     return rank == 0 || i1 >= 0;
@@ -442,11 +445,12 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h, seg;
+      int i, h, h2, seg;
       bool n256;
-      job(c, i, h, n256, seg);  // a missing block loads zero rows (coordinates past the end)
+      job(c, i, h, h2, n256, seg);  // a missing block loads zero rows (coordinates past the end)
       const uint32_t b_bytes = n256 ? B_BYTES : B_BYTES / 2;
       h += seg * p.H;  // the projection's rows of the (fused) weight
+      h2 += seg * p.H;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&bars->empty[rg.s], rg.ph ^ 1);
         if (elect_one()) {
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&bars->full[rg.s], 2 * (A_BYTES + b_bytes));
           tma_load_2d_2sm(st, &xm, &bars->full[rg.s], kb * BK, i * BM);
           if (n256)
-            tma_load_2d_2sm(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, (h + rank) * BN);
+            tma_load_2d_2sm(st + A_BYTES, &wm, &bars->full[rg.s], kb * BK, (rank ? h2 : h) * BN);
           else
             tma_load_2d_2sm(st + A_BYTES, &wm64, &bars->full[rg.s], kb * BK, h * BN + rank * 64);
         }
@@ -472,9 +476,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h, seg;
+      int i, h, h2, seg;
       bool n256;
-      job(c, i, h, n256, seg);
+      job(c, i, h, h2, n256, seg);
       const uint32_t idesc = n256 ? idesc256 : idesc128;
       const int acc = t & 1;
       mbar_wait(&bars->tempty[acc], ((t >> 1) & 1) ^ 1);
@@ -507,9 +511,9 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
     for (int rr = 0; rr * ncl < n_cjobs; ++rr) {
       const int c = job_of(rr);
       if (c >= n_cjobs) continue;
-      int i, h, seg;
+      int i, h, h2, seg;
       bool n256;
-      const bool mine = job(c, i, h, n256, seg);
+      const bool mine = job(c, i, h, h2, n256, seg);
       const int acc = t & 1;
       mbar_wait(&bars->tfull[acc], (t >> 1) & 1);
       tc_fence_after();
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(gemm::NTHREADS, 1)
         __nv_bfloat16* out = seg == 0 ? p.q : (seg == 1 ? p.k_out : p.v_out);
         const bool norm = seg == 0 ? p.norm_w != nullptr : (seg == 1 && p.k_norm != nullptr);
         const bool rope = seg < 2 && p.rope_cos != nullptr;
-        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h, n256 ? h + 1 : -1,
+        gemm::q_epilogue_job(p, tbase + lane_off + acc * Q_BN, r, i, h, n256 ? h2 : -1,
                              nw_u32 + (seg == 1 ? p.H * 128 * 4 : 0), out, norm, rope, release);
       }
       else

@@ -90,9 +90,11 @@ class Plan:
         return self.ws[off:off + 4 * n].view(torch.int32).cpu().numpy().reshape(n_waves, ctas)
 
     def gq_jobs(self):
-        """GEMM-Q CTA-pair jobs (counts[7]): rows (i0, i1 or -1, h, n256); n256
-        jobs cover heads h and h+1, the others head h alone."""
+        """GEMM-Q CTA-pair jobs (counts[7]): rows (i0, i1 or -1, h, n256, h2); n256
+        jobs cover heads h and h2 as one N=256 tile, the others head h alone
+        (h2 = 0)."""
         n = int(self.counts()[7])
         it = self._view(6, torch.int32, 2 * n).view(-1, 2).cpu().numpy()
         x, y = it[:, 0], it[:, 1]
-        return np.stack([x & 0xFFFF, (x >> 16) - 1, y & 0xFF, (y >> 8) & 1], axis=1)
+        return np.stack([x & 0xFFFF, (x >> 16) - 1, y & 0xFF, (y >> 8) & 1, (y >> 16) & 0xFF],
+                        axis=1)
