@@ -404,3 +404,34 @@ def test_fused_qkv_ragged_and_odd_heads(S, H, dm):
             rows = torch.from_numpy(np.repeat(active.T, T, axis=0)[:S]).cuda()
         assert torch.equal(q[rows], q0[rows])
         assert torch.isfinite(k).all() and torch.isfinite(v).all()
+
+
+@pytest.mark.parametrize("H,t", [(1, 9), (2, 5), (5, 33), (17, 40), (24, 258), (64, 12)])
+@pytest.mark.parametrize("ratio", [0.0, 0.3, 0.7, 0.95])
+def test_gq_job_list_invariants(H, t, ratio):
+    """The per-block head pairing covers every active tile exactly once at odd
+    head counts, a single head, 64 heads and every density (including none
+    and all active), and the kernel's output equals the per-head oracle rows."""
+    m = fo()
+    rng = np.random.default_rng(H * 100 + t + int(ratio * 10))
+    active = rng.random((H, t)) >= ratio
+    sym = m.encode_symbols(active, np.ones((H, t, t), bool), 1)
+    if not active.any():
+        return
+    check_gq_jobs(sym.plan(), active)
+    if H * t > 2000:
+        return
+    S, dm = t * T - 37, 256
+    g = torch.Generator(device="cuda").manual_seed(H + t)
+    x = torch.randn(S, dm, device="cuda", generator=g).bfloat16()
+    w_q = (torch.randn(H, dm, T, device="cuda", generator=g) * dm ** -0.5).bfloat16().float()
+    norm = 1 + 0.05 * torch.randn(H, T, device="cuda", generator=g)
+    q = m.project_q(x, w_q, norm, sym, "dispatch", fill=float("nan"))
+    want = oracle.project_q(bf16_np(x), w_q.cpu().numpy(), norm.cpu().numpy(), active, T,
+                            fill=np.nan)
+    got = bf16_np(q)
+    for h in range(H):
+        sel = np.repeat(active[h], T)[:S]
+        if sel.any():
+            assert_bf16_close(got[sel, h], want[h][sel], f"head {h}")
+        assert np.isnan(got[~sel, h]).all()
