@@ -272,6 +272,13 @@ FO_API int fo_rope(const float* x, const float* cos_t, const float* sin_t, int n
                    void* stream);
 FO_API int fo_row_softmax(const float* s, int n, int d, float* out, void* stream);
 
+/* C [m, n] (+)= A [m, k] B [k, n], float32 row-major (accumulate != 0: C += AB,
+ * one rounding of the product then of the sum, like numpy's `c += a @ b`). The
+ * product of the reference-signature GEMM paths at shapes the tcgen05 kernels
+ * do not tile (gemm.py:44-229 with numpy float32 matmul). */
+FO_API int fo_matmul_f32(const float* a, const float* b, float* c, int m, int n, int k,
+                         int accumulate, void* stream);
+
 /* The reference tile-kernel protocol at any block size and head dim, fp32
  * (replaces _kernels/pyref.py:14-48 masked_block_attention and
  * _kernels/_core.pyx:14-101): q, k, v float32 [n, d] (d <= 256); active

@@ -55,6 +55,7 @@ from .gemm import (
     project_qkv,
     rope_tables,
 )
+from .gemm_ref import ReferenceCachedBias
 from .pipeline import (
     HostStepper,
     LayerParams,

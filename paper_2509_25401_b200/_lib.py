@@ -68,6 +68,7 @@ SIGNATURES = {
     "fo_rope": [_P, _P, _P, _I, _I, _P, _P],
     "fo_row_softmax": [_P, _I, _I, _P, _P],
     "fo_masked_block_attention_f32": [_P, _P, _P, _I, _I, _P, _P, _I, _I, _F, _P, _P, _P, _P],
+    "fo_matmul_f32": [_P, _P, _P, _I, _I, _I, _I, _P],
 }
 _RESTYPES = {"fo_last_error": ctypes.c_char_p, "fo_plan_workspace_bytes": _SZ,
              "fo_plan_offsets": None, "fo_policy_workspace_bytes": _SZ,

@@ -833,6 +833,17 @@ int fo_row_softmax(const float* s, int n, int d, float* out, void* stream) {
   return cuda_rc(launch_row_softmax(s, n, d, out, (cudaStream_t)stream), "row_softmax");
 }
 
+int fo_matmul_f32(const float* a, const float* b, float* c, int m, int n, int k, int accumulate,
+                  void* stream) {
+  FO_RANGE();
+  if (!a || !b || !c) return fail(FO_ERR_PARAM, "matmul_f32: null pointer");
+  if (m < 0 || n < 0 || k < 0 || m > 65535 * 64)
+    return fail(FO_ERR_SHAPE, "matmul_f32: m=%d n=%d k=%d", m, n, k);
+  if (m == 0 || n == 0) return FO_OK;
+  return cuda_rc(launch_matmul_f32(a, b, c, m, n, k, accumulate, (cudaStream_t)stream),
+                 "matmul_f32");
+}
+
 int fo_masked_block_attention_f32(const float* q, const float* k, const float* v, int n, int d,
                                   const uint8_t* active, const uint8_t* pair_bits, int b_q, int b_k,
                                   float scale, float* out, unsigned long long* pairs,

@@ -286,6 +286,8 @@ cudaError_t launch_rms_norm(const float* x, const float* w, int n, int d, double
 cudaError_t launch_rope(const float* x, const float* cs, const float* sn, int n, int d, float* out,
                         cudaStream_t st);
 cudaError_t launch_row_softmax(const float* s, int n, int d, float* out, cudaStream_t st);
+cudaError_t launch_matmul_f32(const float* a, const float* b, float* c, int m, int n, int k,
+                              int accumulate, cudaStream_t st);
 cudaError_t launch_masked_block_attention_f32(const float* q, const float* k, const float* v, int n,
                                               int d, const uint8_t* active,
                                               const uint8_t* pair_bits, int b_q, int b_k,

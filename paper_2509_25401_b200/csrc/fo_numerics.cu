@@ -281,6 +281,57 @@ masked_block_attention_f32_kernel(const float* __restrict__ q, const float* __re
     }
   }
 }
+
+// C (+)= A B in fp32, row-major A [m, k], B [k, n], C [m, n]: the product of
+// the reference-signature GEMM paths at shapes the tcgen05 kernels do not tile
+// (gemm.py:44-229 at b_q != 128 or head dims != 128, numpy's float32 matmul).
+// 64 x 64 output tiles, 16 x 16 threads with 4 x 4 outputs each, k in order.
+constexpr int kMmTile = 64, kMmK = 16;
+__global__ void __launch_bounds__(256)
+matmul_f32_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ c,
+                  int m, int n, int k, int accumulate) {
+  __shared__ float as[kMmK][kMmTile + 4];  // A tile transposed: as[kk][row]
+  __shared__ float bs[kMmK][kMmTile];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int r0 = blockIdx.y * kMmTile, c0 = blockIdx.x * kMmTile;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < k; k0 += kMmK) {
+    for (int e = threadIdx.x; e < kMmTile * kMmK; e += 256) {
+      const int rr = e / kMmK, kk = e % kMmK;  // A: 64 rows x 16 k
+      const int gr = r0 + rr, gk = k0 + kk;
+      as[kk][rr] = (gr < m && gk < k) ? a[(size_t)gr * k + gk] : 0.f;
+      const int kb = e / kMmTile, cc = e % kMmTile;  // B: 16 k x 64 cols
+      const int gk2 = k0 + kb, gc = c0 + cc;
+      bs[kb][cc] = (gk2 < k && gc < n) ? b[(size_t)gk2 * n + gc] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kMmK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = as[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = r0 + ty * 4 + i;
+    if (gr >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = c0 + tx * 4 + j;
+      if (gc >= n) continue;
+      float* cp = c + (size_t)gr * n + gc;
+      *cp = accumulate ? __fadd_rn(*cp, acc[i][j]) : acc[i][j];
+    }
+  }
+}
 }  // namespace
 
 // largest row width of the per-row kernels (shared-memory bound)
@@ -370,6 +421,14 @@ cudaError_t launch_masked_block_attention_f32(const float* q, const float* k, co
   else if (d <= 128) FO_MBA(128);
   else FO_MBA(256);
 #undef FO_MBA
+  return cudaGetLastError();
+}
+
+cudaError_t launch_matmul_f32(const float* a, const float* b, float* c, int m, int n, int k,
+                              int accumulate, cudaStream_t st) {
+  note_launch();
+  const dim3 grid((n + kMmTile - 1) / kMmTile, (m + kMmTile - 1) / kMmTile);
+  matmul_f32_kernel<<<grid, 256, 0, st>>>(a, b, c, m, n, k, accumulate);
   return cudaGetLastError();
 }
 

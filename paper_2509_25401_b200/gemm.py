@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, gemm_ref
 from ._runtime import (TILE, Status, as_device, check_bsd, check_finite, check_out, require_cuda,
                        stream_ptr)
 from .attention import check_elapsed, ctypes_floats, forecast_coefficients
@@ -111,7 +111,14 @@ def project_q(x, w_q, norm_weight, symbols, phase, *, b_q=TILE, positions=None, 
     tiles whose cache symbol is 1. Skipped tiles keep `fill` (pass NaN to trap
     illegal reads; fill=None leaves `out` untouched). norm_weight=None skips
     the RMS norm and rope=False the rotary encoding (the plain V projection).
+    The reference's own convention (numpy arrays, one SymbolBuffer per head,
+    any b_q / head dim; out [heads, n, d]) runs gemm_ref.project_q.
     """
+    if not isinstance(w_q, PackedWeight) and gemm_ref.is_reference_call(
+            x, symbols, b_q, np.shape(w_q)[-1]):
+        return gemm_ref.project_q(x, w_q, norm_weight, symbols, phase, b_q=b_q,
+                                  positions=positions, eps=eps, counters=counters,
+                                  fill=0.0 if fill is None else fill)
     require_cuda()
     if phase not in ("update", "dispatch"):
         raise ParameterError(f"unknown phase {phase!r}")
@@ -240,7 +247,13 @@ class CachedBias:
 def project_out_update(o_heads, w_out, symbols_next, cache, order_d, *, b_q=TILE, counters=None,
                        out=None, bias=None, stream=None, status=None, check=True, plan=None):
     """Update-step output projection, two stages in one pass (gemm.py:110-175).
-    Returns (out bf16 [seq, d_model], CachedBias)."""
+    Returns (out bf16 [seq, d_model], CachedBias). The reference's convention
+    (o_heads [heads, n, d], one SymbolBuffer per head, any b_q / head dim)
+    runs gemm_ref.project_out_update and returns its ReferenceCachedBias."""
+    if not isinstance(w_out, PackedWeight) and gemm_ref.is_reference_call(
+            o_heads, symbols_next, b_q, np.shape(w_out)[1]):
+        return gemm_ref.project_out_update(o_heads, w_out, symbols_next, cache, order_d, b_q=b_q,
+                                           counters=counters)
     require_cuda()
     if b_q != TILE:
         raise ParameterError(f"the sm_100a kernels tile blocks of {TILE} tokens")
@@ -304,7 +317,13 @@ def project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n, o
     forecast of the cached-head bias stacks. blocks=(b0, b1) computes only the
     rows of query blocks [b0, b1) (the rest of `out` is untouched) on at most
     max_sms SMs (0 = all): the row chunks the multi-GPU step overlaps with the
-    all-reduce (pipeline.dispatch_step)."""
+    all-reduce (pipeline.dispatch_step). A ReferenceCachedBias or the
+    reference's convention runs gemm_ref.project_out_dispatch."""
+    if isinstance(bias, gemm_ref.ReferenceCachedBias) or (
+            not isinstance(w_out, PackedWeight) and gemm_ref.is_reference_call(
+                o_heads, symbols, b_q, np.shape(w_out)[1])):
+        return gemm_ref.project_out_dispatch(o_heads, w_out, symbols, bias, elapsed_k, interval_n,
+                                             order_d, b_q=b_q, counters=counters)
     require_cuda()
     if b_q != TILE:
         raise ParameterError(f"the sm_100a kernels tile blocks of {TILE} tokens")
